@@ -1,0 +1,172 @@
+/*
+ * bsg.h -- C ABI of the B200-native bijective shuffle (libbsg.so).
+ *
+ * Drop-in boundary for the CPU path of the reference library `bijshuf`
+ * (proj/include/bijshuf/*.hpp).  The reference has no FFI of its own: its
+ * surface is header-only C++ templates.  Each entry point below replaces the
+ * reference function cited beside it, with plain pointers and sizes, no C++
+ * or torch types, and status codes instead of exceptions.  The C++ shim
+ * include/bijshuf_gpu/shuffle.hpp re-exposes the reference's exact names and
+ * signatures (std::vector, ShuffleConfig, exceptions) on top of this ABI.
+ *
+ * Pointers: every data pointer may be host memory (pageable or pinned) or
+ * device memory of the current CUDA device.  Device pointers run
+ * asynchronously on `stream` (a cudaStream_t; NULL = the legacy default
+ * stream).  Host pointers are staged through device buffers owned by the
+ * library and the call returns when the result is back in host memory.
+ * Results are bit-identical to the reference for the same (m, seed, variant,
+ * rounds), independent of `workers` and of any launch geometry.
+ */
+#ifndef BSG_H_
+#define BSG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* Mirrors the reference's exception classes (SURVEY.md 8b "Errors"). */
+typedef enum {
+  BSG_OK = 0,
+  BSG_EINVAL = 1,      /* std::invalid_argument: rounds < 3, bits outside [2,63], derive_round_keys(r<1) */
+  BSG_ERANGE = 2,      /* std::out_of_range: x outside [0, 2^bits) in *_apply / philox_invert */
+  BSG_EALIAS = 3,      /* std::invalid_argument("... out aliases input"), shuffle.hpp:311-312, 356-358 */
+  BSG_ENOMEM = 4,      /* std::bad_alloc */
+  BSG_ECUDA = 5,       /* CUDA runtime error (detail in bsg_last_error()) */
+  BSG_ENODEV = 6,      /* no CUDA device */
+  BSG_EUNSUPPORTED = 7 /* shape this build does not handle (detail in bsg_last_error()) */
+} bsg_status;
+
+/* BijectionVariant, shuffle.hpp:20 */
+typedef enum { BSG_LCG = 0, BSG_VARIABLE_PHILOX = 1 } bsg_variant;
+
+/* ShuffleConfig, shuffle.hpp:25-30.  `workers` is accepted and ignored: the
+ * output never depends on it (shuffle.hpp:22-24). */
+typedef struct {
+  uint64_t seed;
+  int32_t variant;
+  int32_t num_rounds;
+  int32_t workers;
+  int32_t reserved;
+} bsg_config;
+
+/* Default ShuffleConfig{} (seed 0, VariablePhilox, 24 rounds, workers 0). */
+bsg_config bsg_config_default(void);
+
+/* ------------------------------------------------------------ bijections --- */
+/* splitmix.hpp:11-15 */
+uint64_t bsg_mix64(uint64_t z);
+/* splitmix.hpp:22-31 (EINVAL if rounds < 1) */
+bsg_status bsg_derive_round_keys(uint64_t seed, int32_t rounds, uint32_t* keys_out);
+/* shuffle.hpp:49-52 (m >= 2) */
+int32_t bsg_domain_bits(uint64_t m);
+/* make_lcg, bijection.hpp:25-34 */
+bsg_status bsg_make_lcg(int32_t bits, uint64_t seed, uint64_t* a, uint64_t* c);
+/* lcg_apply, bijection.hpp:36-40 (host scalar) */
+bsg_status bsg_lcg_apply(int32_t bits, uint64_t a, uint64_t c, uint64_t x, uint64_t* y);
+/* make_philox + philox_apply / philox_invert, bijection.hpp:73-143 (host scalar) */
+bsg_status bsg_philox_apply(int32_t bits, uint64_t seed, int32_t rounds, uint64_t x, uint64_t* y);
+bsg_status bsg_philox_invert(int32_t bits, uint64_t seed, int32_t rounds, uint64_t y, uint64_t* x);
+/* Batched evaluation on the GPU: y[i] = f(x[i]) (inverse != 0: f^-1).
+ * x == NULL evaluates the counters start .. start+n-1.  ERANGE if an input
+ * lies outside the domain (checked on the host for host inputs only). */
+bsg_status bsg_bijection_apply(int32_t variant, int32_t bits, uint64_t seed, int32_t rounds, int32_t inverse,
+                               const uint64_t* x, uint64_t start, uint64_t* y, uint64_t n, void* stream);
+
+/* --------------------------------------------------------------- shuffle --- */
+/* shuffle_indices / shuffle_indices_into, shuffle.hpp:280-293:
+ * out[k] = sigma(k), the k-th in-range image in counter order. */
+bsg_status bsg_shuffle_indices(uint64_t m, const bsg_config* cfg, uint64_t* out, void* stream);
+/* shuffle_values / shuffle_values_into, shuffle.hpp:298-315:
+ * out[k] = in[sigma(k)] for trivially copyable elements of elem_bytes bytes
+ * (1, 2, 4, 8, 16 natively; any other size through an index pass + byte gather).
+ * EALIAS when out overlaps in. */
+bsg_status bsg_shuffle_values(const void* in, void* out, uint64_t m, uint32_t elem_bytes, const bsg_config* cfg,
+                              void* stream);
+/* `batch` independent shuffles of m elements laid out row-major; shuffle b is
+ * keyed by seed + b (BijectiveShuffleSampler, stats.hpp:314-324). */
+bsg_status bsg_shuffle_values_batched(const void* in, void* out, uint64_t batch, uint64_t m, uint32_t elem_bytes,
+                                      const bsg_config* cfg, void* stream);
+/* gather / gather_into, shuffle.hpp:319-362: out[i] = src[idx[i]] for
+ * i < n; src holds src_len elements.  Indices are not validated (as in the
+ * reference).  EALIAS when out is src or idx (shuffle.hpp:356-358). */
+bsg_status bsg_gather(const void* src, uint64_t src_len, const uint64_t* idx, void* out, uint64_t n,
+                      uint32_t elem_bytes, void* stream);
+
+/* ------------------------------------------- partitioned / multi-GPU path --- */
+/* Up to 16 equally sized input shards (shard g = elements [g*shard_elems,
+ * (g+1)*shard_elems)); pointers may be peer mappings from bsg_ipc_open. */
+typedef struct {
+  const void* ptrs[16];
+  int32_t count;
+  int32_t reserved;
+  uint64_t shard_elems;
+} bsg_shards;
+
+/* One contiguous counter range [counter_begin, counter_end) of the padded
+ * domain of an m-element shuffle: writes the survivors' payload (or images
+ * when in == NULL and in_shards == NULL) to out[0 .. count) in counter order
+ * and stores count to *count_out (device or host pointer; may be NULL).
+ * Concatenating the ranges of a partition of [0, 2^bits) in order yields the
+ * full shuffle: the unit of the multi-GPU scheme. m >= 3. */
+bsg_status bsg_shuffle_range(uint64_t m, const bsg_config* cfg, uint64_t counter_begin, uint64_t counter_end,
+                             const void* in, const bsg_shards* in_shards, void* out, uint32_t elem_bytes,
+                             uint64_t* count_out, void* stream);
+/* Exact number of survivors in [counter_begin, counter_end) (count-only pass;
+ * closed form when m == 2^bits). Host result. */
+bsg_status bsg_range_count(uint64_t m, const bsg_config* cfg, uint64_t counter_begin, uint64_t counter_end,
+                           uint64_t* count, void* stream);
+
+/* All-gather of one u64 per rank (an 8-byte ncclAllGather in practice). */
+typedef int (*bsg_allgather_u64_fn)(const uint64_t* send_one, uint64_t* recv_world, void* user);
+
+/* Rank `rank` of `world` shuffles its contiguous share of the counter domain
+ * (the north-star partition), exchanges survivor counts with `allgather`, and
+ * reports where its piece lands: out[0 .. *local_count) holds global output
+ * positions [*global_offset, *global_offset + *local_count).  Input is either
+ * replicated (`in`, all m elements local) or sharded (`in_shards`, peer
+ * pointers).  Device pointers only. */
+bsg_status bsg_dist_shuffle_values(uint64_t m, const bsg_config* cfg, int32_t rank, int32_t world, const void* in,
+                                   const bsg_shards* in_shards, void* out, uint32_t elem_bytes,
+                                   bsg_allgather_u64_fn allgather, void* user, uint64_t* global_offset,
+                                   uint64_t* local_count, void* stream);
+/* Counter range [begin, end) owned by `rank` of `world` for an m-element shuffle. */
+bsg_status bsg_dist_counter_range(uint64_t m, int32_t rank, int32_t world, uint64_t* begin, uint64_t* end);
+
+/* CUDA IPC helpers for sharded inputs across processes (one process per GPU). */
+#define BSG_IPC_HANDLE_BYTES 64
+bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_HANDLE_BYTES]);
+bsg_status bsg_ipc_open(const unsigned char handle[BSG_IPC_HANDLE_BYTES], void** dev_ptr_out);
+bsg_status bsg_ipc_close(void* dev_ptr);
+
+/* ------------------------------------------------------------ baselines --- */
+/* The paper's SortShuffle (bench.hpp:109-156): random 64-bit
+ * keys mix64(mix64(seed) + i*gamma) and a CUB radix sort of (key, value). */
+bsg_status bsg_sort_shuffle_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t seed, void* stream);
+
+/* --------------------------------------------------------------- utility --- */
+const char* bsg_status_string(bsg_status s);
+/* Detail of the last failure on this thread ("" if none). */
+const char* bsg_last_error(void);
+int32_t bsg_version(void);
+/* Number of kernels this library has launched since load (bench evidence). */
+uint64_t bsg_kernel_launches(void);
+/* Testing knob: 0 = automatic path choice, 1 = always use the compacting
+ * (look-back) kernel even when every image survives. Returns the old value. */
+int32_t bsg_set_force_compact(int32_t on);
+/* Release cached device/host workspaces of the current device. */
+bsg_status bsg_release_workspace(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSG_H_ */

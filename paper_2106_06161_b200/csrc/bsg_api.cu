@@ -1,0 +1,690 @@
+// bsg_api.cu -- the C ABI (include/bsg.h): argument semantics of the
+// reference API, device workspace management, host<->device staging and
+// dispatch to the sm_100a kernels.  No CPU fallback exists: every shuffle,
+// gather and bijection evaluation of the public API runs on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bsg.h"
+#include "bsg_internal.h"
+
+namespace {
+
+using bsg::BijParams;
+
+thread_local std::string t_err;
+
+bsg_status fail(bsg_status s, const std::string& msg) {
+  t_err = msg;
+  return s;
+}
+
+#define BSG_CUDA(expr)                                                                                \
+  do {                                                                                                \
+    cudaError_t _e = (expr);                                                                          \
+    if (_e != cudaSuccess) {                                                                          \
+      if (_e == cudaErrorMemoryAllocation) {                                                          \
+        cudaGetLastError();                                                                           \
+        return fail(BSG_ENOMEM, std::string(#expr) + ": " + cudaGetErrorString(_e));                  \
+      }                                                                                               \
+      return fail(BSG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));                    \
+    }                                                                                                 \
+  } while (0)
+
+#define BSG_TRY(expr)                    \
+  do {                                   \
+    bsg_status _s = (expr);              \
+    if (_s != BSG_OK) return _s;         \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n, bool zero = false) {
+    if (bytes >= n && p) return cudaSuccess;
+    release();
+    size_t want = std::max<size_t>(n, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return e;
+    }
+    bytes = want;
+    if (zero) e = cudaMemset(p, 0, want);
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// Per-device state: look-back workspace, generic-round keys and staging
+// buffers.  All kernels of one device context are ordered through `ws_done`
+// (wait before, record after), so concurrent callers on different streams
+// never share the look-back status words or the key buffer.
+struct DeviceCtx {
+  int device = 0;
+  std::mutex mu;
+  DevBuf status;   // look-back status words (u64 per tile)
+  DevBuf scratch;  // [0] tile counter (u32), [8] count (u64)
+  uint32_t epoch = 0;
+  DevBuf keys;     // round keys for non-24-round Philox
+  DevBuf st_in, st_out, st_idx, st_tmp;  // host-pointer staging / temporaries
+  cudaEvent_t ws_done = nullptr;
+  bool ready = false;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
+int g_force_compact = 0;
+
+bsg_status current_ctx(DeviceCtx** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BSG_ENODEV, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (static_cast<int>(g_ctx.size()) <= dev) g_ctx.resize(dev + 1);
+  if (!g_ctx[dev]) {
+    g_ctx[dev] = std::make_unique<DeviceCtx>();
+    g_ctx[dev]->device = dev;
+  }
+  DeviceCtx* c = g_ctx[dev].get();
+  if (!c->ready) {
+    BSG_CUDA(cudaEventCreateWithFlags(&c->ws_done, cudaEventDisableTiming));
+    BSG_CUDA(c->scratch.ensure(64, true));
+    c->ready = true;
+  }
+  *out = c;
+  return BSG_OK;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  const char* x = static_cast<const char*>(a);
+  const char* y = static_cast<const char*>(b);
+  return an && bn && x < y + bn && y < x + an;
+}
+
+bsg_config resolve_cfg(const bsg_config* cfg) { return cfg ? *cfg : bsg_config_default(); }
+
+// make_lcg / make_philox checks (bijection.hpp:26-27, 75-78), message text
+// following the reference exceptions.
+bsg_status build_params(int variant, int bits, uint64_t seed, int rounds, BijParams& p) {
+  if (variant != bsg::kLcg && variant != bsg::kPhilox) return fail(BSG_EINVAL, "unknown bijection variant");
+  if (bsg::make_params(variant, bits, seed, rounds, p) != 0) {
+    if (variant == bsg::kLcg) return fail(BSG_EINVAL, "modulus_bits must be in [1, 63]");
+    if (bits < 2 || bits > 63) return fail(BSG_EINVAL, "total_bits must be in [2, 63]");
+    return fail(BSG_EINVAL, "num_rounds must be >= 3");
+  }
+  return BSG_OK;
+}
+
+// Orders this call after every earlier kernel of the context (any stream).
+bsg_status ws_begin(DeviceCtx* c, cudaStream_t s) {
+  BSG_CUDA(cudaStreamWaitEvent(s, c->ws_done, 0));
+  return BSG_OK;
+}
+bsg_status ws_end(DeviceCtx* c, cudaStream_t s) {
+  BSG_CUDA(cudaEventRecord(c->ws_done, s));
+  return BSG_OK;
+}
+
+// Uploads the key schedule for generic-round Philox kernels.
+bsg_status upload_keys(DeviceCtx* c, BijParams& p, uint64_t seed, cudaStream_t s) {
+  if (p.variant != bsg::kPhilox || p.rounds == 24) return BSG_OK;
+  std::vector<uint32_t> k(static_cast<size_t>(p.rounds));
+  for (int i = 0; i < p.rounds; ++i) k[i] = bsg::round_key(seed, i);
+  BSG_CUDA(c->keys.ensure(k.size() * 4));
+  BSG_CUDA(cudaMemcpyAsync(c->keys.p, k.data(), k.size() * 4, cudaMemcpyHostToDevice, s));
+  BSG_CUDA(cudaStreamSynchronize(s));  // k is a stack temporary
+  p.gkeys = static_cast<const uint32_t*>(c->keys.p);
+  return BSG_OK;
+}
+
+// Prepares the look-back workspace for a compacting launch over `tiles`.
+bsg_status lookback_prepare(DeviceCtx* c, uint64_t tiles, cudaStream_t s, bsg::Lookback& lb) {
+  const size_t need = std::max<uint64_t>(tiles, 1) * sizeof(unsigned long long);
+  if (c->status.bytes < need) {
+    BSG_CUDA(cudaStreamSynchronize(s));
+    BSG_CUDA(c->status.ensure(need, true));
+    c->epoch = 0;
+  }
+  if (++c->epoch >= (1u << 22)) {  // epoch wrap: clear stale words once
+    BSG_CUDA(cudaMemsetAsync(c->status.p, 0, c->status.bytes, s));
+    c->epoch = 1;
+  }
+  lb.status = static_cast<unsigned long long*>(c->status.p);
+  lb.tile_counter = static_cast<unsigned int*>(c->scratch.p);
+  lb.epoch = c->epoch;
+  return BSG_OK;
+}
+
+int native_code(uint32_t eb, const void* a, const void* b) {
+  if (eb != 1 && eb != 2 && eb != 4 && eb != 8 && eb != 16) return -1;
+  const uintptr_t al = eb;
+  if ((reinterpret_cast<uintptr_t>(a) % al) || (reinterpret_cast<uintptr_t>(b) % al)) return -1;
+  return static_cast<int>(eb);
+}
+
+// Device-pointer core: range [c0, c1) of an m >= 3 shuffle.  elem_code 0 =
+// indices.  count_dev (device) receives the survivor count when non-null.
+bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c0, uint64_t c1, const bsg::Src& src,
+                     void* out, int elem_code, unsigned long long* count_dev, cudaStream_t s) {
+  const int bits = bsg::domain_bits(m);
+  BijParams p;
+  BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, p));
+  BSG_TRY(ws_begin(c, s));
+  BSG_TRY(upload_keys(c, p, cfg.seed, s));
+  const bool pow2 = (m == (1ULL << bits));
+  bsg::ShuffleLaunch L;
+  L.src = src;
+  L.out = out;
+  L.m = m;
+  L.c0 = c0;
+  L.c1 = c1;
+  L.p = p;
+  L.compact = !pow2 || g_force_compact;
+  L.count_out = count_dev;
+  if (L.compact) {
+    const uint64_t tile = bsg::kCompactTile;
+    BSG_TRY(lookback_prepare(c, (c1 - c0 + tile - 1) / tile, s, L.lb));
+  }
+  if (c1 > c0) BSG_CUDA(bsg::launch_shuffle(elem_code, L, s));
+  if (count_dev && (!L.compact || c1 == c0)) {
+    const unsigned long long n = c1 - c0;
+    BSG_CUDA(cudaMemcpyAsync(count_dev, &n, sizeof(n), cudaMemcpyHostToDevice, s));
+    BSG_CUDA(cudaStreamSynchronize(s));
+  }
+  return ws_end(c, s);
+}
+
+// Device-pointer shuffle of m elements (all sizes, m >= 0).
+bsg_status shuffle_device(DeviceCtx* c, const void* in, void* out, uint64_t m, uint32_t eb, const bsg_config& cfg,
+                          cudaStream_t s) {
+  if (m == 0) return BSG_OK;
+  const bool idx = (in == nullptr);
+  const size_t ob = idx ? 8 : eb;
+  if (m <= 2) {  // shuffle.hpp:228-240 / 249-259: variant and rounds ignored
+    const uint64_t bit = (m == 2) ? (bsg::mix64(cfg.seed) & 1) : 0;
+    if (idx) {
+      const uint64_t v[2] = {bit, bit ^ 1};
+      BSG_CUDA(cudaMemcpyAsync(out, v, m * 8, cudaMemcpyHostToDevice, s));
+      BSG_CUDA(cudaStreamSynchronize(s));
+    } else {
+      for (uint64_t k = 0; k < m; ++k)
+        BSG_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + k * ob, static_cast<const char*>(in) + (k ^ bit) * eb, eb,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    return BSG_OK;
+  }
+  bsg::Src src;
+  src.base = in;
+  const int bits = bsg::domain_bits(m);
+  const uint64_t n = (bits >= 64) ? 0 : (1ULL << bits);
+  if (bits > 63) return fail(BSG_EINVAL, cfg.variant == bsg::kLcg ? "modulus_bits must be in [1, 63]"
+                                                                     : "total_bits must be in [2, 63]");
+  if (idx) return run_range(c, m, cfg, 0, n, src, out, 0, nullptr, s);
+  const int code = native_code(eb, in, out);
+  if (code > 0) return run_range(c, m, cfg, 0, n, src, out, code, nullptr, s);
+  // Other element sizes: permutation first, then a record gather.
+  BSG_CUDA(c->st_idx.ensure(m * 8));
+  BSG_TRY(run_range(c, m, cfg, 0, n, bsg::Src{}, c->st_idx.p, 0, nullptr, s));
+  BSG_TRY(ws_begin(c, s));
+  BSG_CUDA(bsg::launch_gather_bytes(in, static_cast<const uint64_t*>(c->st_idx.p), out, m, eb, s));
+  return ws_end(c, s);
+}
+
+template <typename Fn>
+bsg_status with_ctx(Fn&& fn) {
+  DeviceCtx* c = nullptr;
+  BSG_TRY(current_ctx(&c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  t_err.clear();
+  return fn(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+bsg_config bsg_config_default(void) {
+  bsg_config c;
+  c.seed = 0;
+  c.variant = BSG_VARIABLE_PHILOX;
+  c.num_rounds = 24;
+  c.workers = 0;
+  c.reserved = 0;
+  return c;
+}
+
+uint64_t bsg_mix64(uint64_t z) { return bsg::mix64(z); }
+
+bsg_status bsg_derive_round_keys(uint64_t seed, int32_t rounds, uint32_t* keys_out) {
+  if (rounds < 1) return fail(BSG_EINVAL, "num_rounds must be >= 1");
+  for (int i = 0; i < rounds; ++i) keys_out[i] = bsg::round_key(seed, i);
+  return BSG_OK;
+}
+
+int32_t bsg_domain_bits(uint64_t m) { return bsg::domain_bits(m); }
+
+bsg_status bsg_make_lcg(int32_t bits, uint64_t seed, uint64_t* a, uint64_t* c) {
+  BijParams p;
+  BSG_TRY(build_params(bsg::kLcg, bits, seed, 0, p));
+  *a = p.lcg_a;
+  *c = p.lcg_c;
+  return BSG_OK;
+}
+
+bsg_status bsg_lcg_apply(int32_t bits, uint64_t a, uint64_t c, uint64_t x, uint64_t* y) {
+  const uint64_t mask = bits >= 64 ? ~0ULL : ((1ULL << bits) - 1);  // LcgParams::domain_mask
+  if (x > mask) return fail(BSG_ERANGE, "lcg_apply: x outside [0, 2^bits)");
+  *y = (a * x + c) & mask;
+  return BSG_OK;
+}
+
+bsg_status bsg_philox_apply(int32_t bits, uint64_t seed, int32_t rounds, uint64_t x, uint64_t* y) {
+  BijParams p;
+  BSG_TRY(build_params(bsg::kPhilox, bits, seed, rounds, p));
+  if ((x >> bits) != 0) return fail(BSG_ERANGE, "philox_apply: x outside [0, 2^total_bits)");
+  *y = bsg::host_apply(p, seed, x, false);
+  return BSG_OK;
+}
+
+bsg_status bsg_philox_invert(int32_t bits, uint64_t seed, int32_t rounds, uint64_t y, uint64_t* x) {
+  BijParams p;
+  BSG_TRY(build_params(bsg::kPhilox, bits, seed, rounds, p));
+  if ((y >> bits) != 0) return fail(BSG_ERANGE, "philox_invert: y outside [0, 2^total_bits)");
+  *x = bsg::host_apply(p, seed, y, true);
+  return BSG_OK;
+}
+
+bsg_status bsg_bijection_apply(int32_t variant, int32_t bits, uint64_t seed, int32_t rounds, int32_t inverse,
+                               const uint64_t* x, uint64_t start, uint64_t* y, uint64_t n, void* stream) {
+  BijParams p;
+  BSG_TRY(build_params(variant, bits, seed, rounds, p));
+  if (n == 0) return BSG_OK;
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    const bool xd = x && is_device_ptr(x), yd = is_device_ptr(y);
+    if (x && !xd) {
+      for (uint64_t i = 0; i < n; ++i)
+        if (x[i] > p.mask) return fail(BSG_ERANGE, "bijection_apply: x outside [0, 2^bits)");
+    } else if (!x && (start > p.mask || n - 1 > p.mask - start)) {
+      return fail(BSG_ERANGE, "bijection_apply: counters outside [0, 2^bits)");
+    }
+    const uint64_t* dx = x;
+    uint64_t* dy = y;
+    if (x && !xd) {
+      BSG_CUDA(c->st_in.ensure(n * 8));
+      BSG_CUDA(cudaMemcpyAsync(c->st_in.p, x, n * 8, cudaMemcpyHostToDevice, s));
+      dx = static_cast<const uint64_t*>(c->st_in.p);
+    }
+    if (!yd) {
+      BSG_CUDA(c->st_out.ensure(n * 8));
+      dy = static_cast<uint64_t*>(c->st_out.p);
+    }
+    BSG_TRY(ws_begin(c, s));
+    BSG_TRY(upload_keys(c, p, seed, s));
+    BSG_CUDA(bsg::launch_map(dx, dy, n, start, p, inverse != 0, s));
+    BSG_TRY(ws_end(c, s));
+    if (!yd) {
+      BSG_CUDA(cudaMemcpyAsync(y, dy, n * 8, cudaMemcpyDeviceToHost, s));
+      BSG_CUDA(cudaStreamSynchronize(s));
+    }
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_shuffle_indices(uint64_t m, const bsg_config* cfg_in, uint64_t* out, void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (m == 0) return BSG_OK;
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (is_device_ptr(out)) return shuffle_device(c, nullptr, out, m, 8, cfg, s);
+    BSG_CUDA(c->st_out.ensure(m * 8));
+    BSG_TRY(shuffle_device(c, nullptr, c->st_out.p, m, 8, cfg, s));
+    BSG_CUDA(cudaMemcpyAsync(out, c->st_out.p, m * 8, cudaMemcpyDeviceToHost, s));
+    BSG_CUDA(cudaStreamSynchronize(s));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_shuffle_values(const void* in, void* out, uint64_t m, uint32_t elem_bytes, const bsg_config* cfg_in,
+                              void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (in != nullptr && in == out) return fail(BSG_EALIAS, "shuffle_values_into: out aliases input");
+  if (m == 0) return BSG_OK;
+  if (elem_bytes == 0) return fail(BSG_EINVAL, "elem_bytes must be >= 1");
+  if (!in || !out) return fail(BSG_EINVAL, "null pointer");
+  const size_t bytes = m * static_cast<size_t>(elem_bytes);
+  if (overlaps(in, bytes, out, bytes)) return fail(BSG_EALIAS, "shuffle_values_into: out aliases input");
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    const bool din = is_device_ptr(in), dout = is_device_ptr(out);
+    if (din && dout) return shuffle_device(c, in, out, m, elem_bytes, cfg, s);
+    const void* di = in;
+    void* dO = out;
+    if (!din) {
+      BSG_CUDA(c->st_in.ensure(bytes));
+      BSG_CUDA(cudaMemcpyAsync(c->st_in.p, in, bytes, cudaMemcpyHostToDevice, s));
+      di = c->st_in.p;
+    }
+    if (!dout) {
+      BSG_CUDA(c->st_out.ensure(bytes));
+      dO = c->st_out.p;
+    }
+    BSG_TRY(shuffle_device(c, di, dO, m, elem_bytes, cfg, s));
+    if (!dout) BSG_CUDA(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDeviceToHost, s));
+    BSG_CUDA(cudaStreamSynchronize(s));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_shuffle_values_batched(const void* in, void* out, uint64_t batch, uint64_t m, uint32_t elem_bytes,
+                                      const bsg_config* cfg_in, void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (in != nullptr && in == out) return fail(BSG_EALIAS, "shuffle_values_batched: out aliases input");
+  if (m == 0 || batch == 0) return BSG_OK;
+  if (elem_bytes == 0) return fail(BSG_EINVAL, "elem_bytes must be >= 1");
+  if (!in || !out) return fail(BSG_EINVAL, "null pointer");
+  const size_t bytes = batch * m * static_cast<size_t>(elem_bytes);
+  if (overlaps(in, bytes, out, bytes)) return fail(BSG_EALIAS, "shuffle_values_batched: out aliases input");
+  const int bits = bsg::domain_bits(m);
+  if (m >= 3) {
+    BijParams p;
+    BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, p));
+  }
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    const bool din = is_device_ptr(in), dout = is_device_ptr(out);
+    const void* di = in;
+    void* dO = out;
+    if (!din) {
+      BSG_CUDA(c->st_in.ensure(bytes));
+      BSG_CUDA(cudaMemcpyAsync(c->st_in.p, in, bytes, cudaMemcpyHostToDevice, s));
+      di = c->st_in.p;
+    }
+    if (!dout) {
+      BSG_CUDA(c->st_out.ensure(bytes));
+      dO = c->st_out.p;
+    }
+    const int code = native_code(elem_bytes, di, dO);
+    if (m >= 3 && code > 0 && bsg::batched_supported(code, static_cast<uint32_t>(m), bits, cfg.num_rounds)) {
+      bsg::BatchedLaunch B;
+      B.in = di;
+      B.out = dO;
+      B.batch = batch;
+      B.m = static_cast<uint32_t>(m);
+      B.seed = cfg.seed;
+      BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, B.p));
+      BSG_TRY(ws_begin(c, s));
+      BSG_CUDA(bsg::launch_batched(code, B, s));
+      BSG_TRY(ws_end(c, s));
+    } else {
+      const size_t row = m * static_cast<size_t>(elem_bytes);
+      for (uint64_t b = 0; b < batch; ++b) {
+        bsg_config cb = cfg;
+        cb.seed = cfg.seed + b;
+        BSG_TRY(shuffle_device(c, static_cast<const char*>(di) + b * row, static_cast<char*>(dO) + b * row, m,
+                               elem_bytes, cb, s));
+      }
+    }
+    if (!dout) BSG_CUDA(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDeviceToHost, s));
+    if (!din || !dout) BSG_CUDA(cudaStreamSynchronize(s));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_gather(const void* src, uint64_t src_len, const uint64_t* idx, void* out, uint64_t n,
+                      uint32_t elem_bytes, void* stream) {
+  if (out != nullptr && (out == src || out == static_cast<const void*>(idx)))
+    return fail(BSG_EALIAS, "gather_into: out aliases an input");
+  if (n == 0) return BSG_OK;
+  if (elem_bytes == 0 || !src || !idx || !out) return fail(BSG_EINVAL, "invalid gather arguments");
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    const bool ds = is_device_ptr(src), di = is_device_ptr(idx), dout = is_device_ptr(out);
+    const void* S = src;
+    const uint64_t* I = idx;
+    void* O = out;
+    const size_t sb = src_len * static_cast<size_t>(elem_bytes), ob = n * static_cast<size_t>(elem_bytes);
+    if (!ds) {
+      BSG_CUDA(c->st_in.ensure(sb));
+      BSG_CUDA(cudaMemcpyAsync(c->st_in.p, src, sb, cudaMemcpyHostToDevice, s));
+      S = c->st_in.p;
+    }
+    if (!di) {
+      BSG_CUDA(c->st_idx.ensure(n * 8));
+      BSG_CUDA(cudaMemcpyAsync(c->st_idx.p, idx, n * 8, cudaMemcpyHostToDevice, s));
+      I = static_cast<const uint64_t*>(c->st_idx.p);
+    }
+    if (!dout) {
+      BSG_CUDA(c->st_out.ensure(ob));
+      O = c->st_out.p;
+    }
+    BSG_TRY(ws_begin(c, s));
+    const int code = native_code(elem_bytes, S, O);
+    if (code > 0) BSG_CUDA(bsg::launch_gather(code, S, I, O, n, s));
+    else BSG_CUDA(bsg::launch_gather_bytes(S, I, O, n, elem_bytes, s));
+    BSG_TRY(ws_end(c, s));
+    if (!dout) BSG_CUDA(cudaMemcpyAsync(out, O, ob, cudaMemcpyDeviceToHost, s));
+    if (!ds || !di || !dout) BSG_CUDA(cudaStreamSynchronize(s));
+    return BSG_OK;
+  });
+}
+
+static bsg_status make_src(const void* in, const bsg_shards* sh, uint64_t m, bsg::Src& src) {
+  src = bsg::Src{};
+  if (sh && sh->count > 0) {
+    if (sh->count > bsg::kMaxShards) return fail(BSG_EINVAL, "at most 16 input shards");
+    if (sh->shard_elems == 0 || static_cast<uint64_t>(sh->count) * sh->shard_elems < m)
+      return fail(BSG_EINVAL, "input shards do not cover m elements");
+    for (int g = 0; g < sh->count; ++g) src.shard[g] = sh->ptrs[g];
+    src.nshards = sh->count;
+    src.shard_elems = sh->shard_elems;
+    src.shard_shift = -1;
+    if ((sh->shard_elems & (sh->shard_elems - 1)) == 0) {
+      int sft = 0;
+      while ((1ULL << sft) < sh->shard_elems) ++sft;
+      src.shard_shift = sft;
+    }
+  } else {
+    src.base = in;
+  }
+  return BSG_OK;
+}
+
+bsg_status bsg_shuffle_range(uint64_t m, const bsg_config* cfg_in, uint64_t counter_begin, uint64_t counter_end,
+                             const void* in, const bsg_shards* in_shards, void* out, uint32_t elem_bytes,
+                             uint64_t* count_out, void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (m < 3) return fail(BSG_EINVAL, "shuffle_range needs m >= 3 (m <= 2 has no padded domain)");
+  const int bits = bsg::domain_bits(m);
+  BijParams p;
+  BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, p));
+  const uint64_t n = 1ULL << bits;
+  if (counter_begin > counter_end || counter_end > n) return fail(BSG_ERANGE, "counter range outside [0, 2^bits)");
+  const bool indices = (in == nullptr) && (in_shards == nullptr || in_shards->count == 0);
+  bsg::Src src;
+  BSG_TRY(make_src(in, in_shards, m, src));
+  int code = 0;
+  if (!indices) {
+    code = native_code(elem_bytes, src.nshards ? src.shard[0] : in, out);
+    if (code < 0) return fail(BSG_EUNSUPPORTED, "shuffle_range: elem_bytes must be 1, 2, 4, 8 or 16 (aligned)");
+  }
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (!is_device_ptr(out)) return fail(BSG_EINVAL, "shuffle_range: out must be device memory");
+    const bool count_dev = count_out && is_device_ptr(count_out);
+    unsigned long long* cd =
+        count_dev ? reinterpret_cast<unsigned long long*>(count_out)
+                  : reinterpret_cast<unsigned long long*>(static_cast<char*>(c->scratch.p) + 8);
+    BSG_TRY(run_range(c, m, cfg, counter_begin, counter_end, src, out, code, cd, s));
+    if (count_out && !count_dev) {
+      BSG_CUDA(cudaMemcpyAsync(count_out, cd, 8, cudaMemcpyDeviceToHost, s));
+      BSG_CUDA(cudaStreamSynchronize(s));
+    }
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_range_count(uint64_t m, const bsg_config* cfg_in, uint64_t counter_begin, uint64_t counter_end,
+                           uint64_t* count, void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (m < 3) return fail(BSG_EINVAL, "range_count needs m >= 3");
+  const int bits = bsg::domain_bits(m);
+  BijParams p;
+  BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, p));
+  const uint64_t n = 1ULL << bits;
+  if (counter_begin > counter_end || counter_end > n) return fail(BSG_ERANGE, "counter range outside [0, 2^bits)");
+  if (m == n) {
+    *count = counter_end - counter_begin;
+    return BSG_OK;
+  }
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    auto* cd = reinterpret_cast<unsigned long long*>(static_cast<char*>(c->scratch.p) + 8);
+    BSG_TRY(ws_begin(c, s));
+    BSG_TRY(upload_keys(c, p, cfg.seed, s));
+    BSG_CUDA(bsg::launch_count(m, counter_begin, counter_end, p, cd, s));
+    BSG_TRY(ws_end(c, s));
+    BSG_CUDA(cudaMemcpyAsync(count, cd, 8, cudaMemcpyDeviceToHost, s));
+    BSG_CUDA(cudaStreamSynchronize(s));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_dist_counter_range(uint64_t m, int32_t rank, int32_t world, uint64_t* begin, uint64_t* end) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(BSG_EINVAL, "rank/world out of range");
+  if (m < 3) return fail(BSG_EINVAL, "distributed shuffle needs m >= 3");
+  const int bits = bsg::domain_bits(m);
+  if (bits > 63) return fail(BSG_EINVAL, "total_bits must be in [2, 63]");
+  const uint64_t n = 1ULL << bits;
+  const uint64_t base = n / world, rem = n % world;
+  *begin = rank * base + std::min<uint64_t>(rank, rem);
+  *end = *begin + base + (static_cast<uint64_t>(rank) < rem ? 1 : 0);
+  return BSG_OK;
+}
+
+bsg_status bsg_dist_shuffle_values(uint64_t m, const bsg_config* cfg_in, int32_t rank, int32_t world, const void* in,
+                                   const bsg_shards* in_shards, void* out, uint32_t elem_bytes,
+                                   bsg_allgather_u64_fn allgather, void* user, uint64_t* global_offset,
+                                   uint64_t* local_count, void* stream) {
+  if (!allgather) return fail(BSG_EINVAL, "allgather callback required");
+  uint64_t b = 0, e = 0;
+  BSG_TRY(bsg_dist_counter_range(m, rank, world, &b, &e));
+  uint64_t cnt = 0;
+  BSG_TRY(bsg_shuffle_range(m, cfg_in, b, e, in, in_shards, out, elem_bytes, &cnt, stream));
+  std::vector<uint64_t> all(static_cast<size_t>(world), 0);
+  if (allgather(&cnt, all.data(), user) != 0) return fail(BSG_ECUDA, "allgather callback failed");
+  uint64_t off = 0, tot = 0;
+  for (int r = 0; r < world; ++r) {
+    if (r < rank) off += all[r];
+    tot += all[r];
+  }
+  if (tot != m) return fail(BSG_ECUDA, "survivor counts do not sum to m (inconsistent ranks?)");
+  *global_offset = off;
+  *local_count = cnt;
+  return BSG_OK;
+}
+
+bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_HANDLE_BYTES]) {
+  cudaIpcMemHandle_t h;
+  BSG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) <= BSG_IPC_HANDLE_BYTES, "ipc handle size");
+  std::memset(handle_out, 0, BSG_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return BSG_OK;
+}
+
+bsg_status bsg_ipc_open(const unsigned char handle[BSG_IPC_HANDLE_BYTES], void** dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  BSG_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return BSG_OK;
+}
+
+bsg_status bsg_ipc_close(void* dev_ptr) {
+  BSG_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return BSG_OK;
+}
+
+bsg_status bsg_sort_shuffle_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t seed, void* stream) {
+  if (n == 0) return BSG_OK;
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (!is_device_ptr(in) || !is_device_ptr(out)) return fail(BSG_EINVAL, "sort_shuffle: device pointers only");
+    size_t need = 0;
+    BSG_CUDA(bsg::sort_shuffle_u64(in, out, n, seed, nullptr, &need, s));
+    BSG_CUDA(c->st_tmp.ensure(need));
+    size_t have = c->st_tmp.bytes;
+    BSG_TRY(ws_begin(c, s));
+    BSG_CUDA(bsg::sort_shuffle_u64(in, out, n, seed, c->st_tmp.p, &have, s));
+    return ws_end(c, s);
+  });
+}
+
+const char* bsg_status_string(bsg_status s) {
+  switch (s) {
+    case BSG_OK: return "ok";
+    case BSG_EINVAL: return "invalid argument";
+    case BSG_ERANGE: return "out of range";
+    case BSG_EALIAS: return "output aliases input";
+    case BSG_ENOMEM: return "out of memory";
+    case BSG_ECUDA: return "CUDA error";
+    case BSG_ENODEV: return "no CUDA device";
+    case BSG_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* bsg_last_error(void) { return t_err.c_str(); }
+
+int32_t bsg_version(void) { return 100; }
+
+uint64_t bsg_kernel_launches(void) { return bsg::launches(); }
+
+int32_t bsg_set_force_compact(int32_t on) {
+  const int old = g_force_compact;
+  g_force_compact = on ? 1 : 0;
+  return old;
+}
+
+bsg_status bsg_release_workspace(void) {
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    BSG_CUDA(cudaDeviceSynchronize());
+    c->status.release();
+    c->keys.release();
+    c->st_in.release();
+    c->st_out.release();
+    c->st_idx.release();
+    c->st_tmp.release();
+    c->epoch = 0;
+    return BSG_OK;
+  });
+}
+
+}  // extern "C"

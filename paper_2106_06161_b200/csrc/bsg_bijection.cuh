@@ -1,0 +1,230 @@
+// bsg_bijection.cuh -- the keyed bijections of the bijective shuffle, as
+// register-resident 32-bit integer arithmetic for sm_100a (and the same
+// functions on the host for key schedules and scalar evaluation).
+//
+// Semantics follow the reference bit for bit:
+//   mix64 / derive_round_keys ........ proj/include/bijshuf/splitmix.hpp:11-31
+//   make_lcg / lcg_apply .............. bijection.hpp:25-40 (engine form shuffle.hpp:157-162)
+//   make_philox / philox_apply ........ bijection.hpp:73-111 (engine form shuffle.hpp:71-86)
+//   philox_invert / odd_inverse ....... bijection.hpp:61-65, 117-143
+//   shuffle_domain_bits ............... shuffle.hpp:49-52
+//
+// Why 32-bit state is exact: the reference keeps s0 (left, L = floor(bits/2)
+// <= 31 bits) and s1 (right, R <= 32 bits) in u64 and multiplies by the
+// 64-bit constant M0.  Only hi = (M0*s0 mod 2^64) >> 32 and lo = M0*s0 mod
+// 2^32 are used, and with s0 < 2^31:
+//     lo = s0 * M0lo (mod 2^32),  hi = umulhi(s0, M0lo) + s0 * M0hi (mod 2^32).
+// The unbalanced-split shift (lo << d) is folded into the multiplier
+// (M0lo << d), and `lo & right_mask` drops the bit the u64 shift would keep.
+// All state therefore lives in 32-bit registers; only the counter/image are
+// 64-bit when bits > 32.  Round keys are kernel parameters (constant bank),
+// so every round is IMAD.HI + IMAD + IMAD + LOP3s with c[][] operands.
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define BSG_HD __host__ __device__ __forceinline__
+#else
+#define BSG_HD inline
+#endif
+
+namespace bsg {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;  // splitmix.hpp:18
+constexpr uint64_t kM0 = 0xD2B74407B1CE6E93ULL;     // bijection.hpp:57
+constexpr uint32_t kM0Lo = static_cast<uint32_t>(kM0);
+constexpr uint32_t kM0Hi = static_cast<uint32_t>(kM0 >> 32);
+
+constexpr uint64_t odd_inverse_pow2_64(uint64_t a) {  // bijection.hpp:61-65
+  uint64_t x = a;
+  for (int i = 0; i < 5; ++i) x *= 2 - a * x;
+  return x;
+}
+constexpr uint64_t kM0Inv = odd_inverse_pow2_64(kM0);
+constexpr uint32_t kM0InvLo = static_cast<uint32_t>(kM0Inv);
+static_assert(kM0Inv * kM0 == 1ULL, "M0 inverse");
+
+BSG_HD uint64_t mix64(uint64_t z) {  // splitmix.hpp:11-15
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+BSG_HD uint32_t round_key(uint64_t seed, int i) {  // splitmix.hpp:27-28
+  return static_cast<uint32_t>(mix64(seed + (static_cast<uint64_t>(i) + 1) * kGamma));
+}
+
+// shuffle.hpp:49-52: max(4, ceil(log2 m)) for m >= 2.
+BSG_HD int domain_bits(uint64_t m) {
+  int needed = 0;
+  if (m > 1) {
+    uint64_t v = m - 1;
+    while (v) {
+      ++needed;
+      v >>= 1;
+    }
+  }
+  return needed < 4 ? 4 : needed;
+}
+
+enum Variant : int32_t { kLcg = 0, kPhilox = 1 };
+
+// Number of round keys carried inside the kernel parameter block.  Rounds
+// beyond this read a device array (the generic path).
+constexpr int kParamKeys = 32;
+
+// Everything a kernel needs to evaluate the bijection of one shuffle.
+struct BijParams {
+  uint64_t lcg_a = 1, lcg_c = 0, lcg_ainv = 1;  // LCG (a forced odd), inverse multiplier
+  uint64_t mask = 0;                            // 2^bits - 1
+  uint32_t LM = 0, RM = 0;                      // Philox half masks (RM may be 0xFFFFFFFF)
+  int32_t variant = kPhilox, bits = 0, L = 0, R = 0, rounds = 0, pad = 0;
+  const uint32_t* gkeys = nullptr;  // device copy of all keys (rounds > kParamKeys)
+  uint32_t keys[kParamKeys] = {};
+};
+
+// ---------------------------------------------------------------------------
+// Philox rounds on split state (s0 < 2^L, s1 < 2^R).  D = R - L in {0, 1}.
+// For D == 0 the right half may carry garbage above bit R between rounds:
+// it only enters `(hi ^ k ^ s1) & LM`, so it is masked once at the end.
+// ---------------------------------------------------------------------------
+template <int D>
+BSG_HD void philox_round(uint32_t& s0, uint32_t& s1, uint32_t k, int L, uint32_t LM, uint32_t RM) {
+#ifdef __CUDA_ARCH__
+  const uint32_t hi = __umulhi(s0, kM0Lo) + s0 * kM0Hi;
+#else
+  const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(s0) * kM0Lo) >> 32) + s0 * kM0Hi;
+#endif
+  uint32_t lo = s0 * (kM0Lo << D);
+  if (D) lo |= s1 >> L;
+  s0 = (hi ^ k ^ s1) & LM;
+  s1 = D ? (lo & RM) : lo;
+}
+
+// Inverse round (bijection.hpp:127-141).  For D == 1 the right half carries
+// garbage above bit L+1 between rounds (masked at the end): the spare bit is
+// bit 0 and only `t1 >> 1` modulo 2^L is consumed.
+template <int D>
+BSG_HD void philox_inv_round(uint32_t& t0, uint32_t& t1, uint32_t k, int L, uint32_t LM) {
+  const uint32_t s0 = ((t1 >> D) * kM0InvLo) & LM;
+#ifdef __CUDA_ARCH__
+  const uint32_t hi = __umulhi(s0, kM0Lo) + s0 * kM0Hi;
+#else
+  const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(s0) * kM0Lo) >> 32) + s0 * kM0Hi;
+#endif
+  const uint32_t s1 = ((hi ^ k ^ t0) & LM) | (D ? (t1 << L) : 0u);
+  t0 = s0;
+  t1 = s1;
+}
+
+// Key access: compile-time round count NR > 0 reads the parameter block with
+// constant indices; NR == 0 loops over p.rounds keys from p.gkeys (device) or
+// p.keys (host, rounds <= kParamKeys) -- the generic path.
+template <int D, int NR>
+BSG_HD uint64_t philox_fwd(uint64_t x, const BijParams& p) {
+  uint32_t s0 = static_cast<uint32_t>(x >> p.R);
+  uint32_t s1 = static_cast<uint32_t>(x) & p.RM;
+  if constexpr (NR > 0) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) philox_round<D>(s0, s1, p.keys[i], p.L, p.LM, p.RM);
+  } else {
+#ifdef __CUDA_ARCH__
+    const uint32_t* ks = p.gkeys;
+#pragma unroll 4
+    for (int i = 0; i < p.rounds; ++i) philox_round<D>(s0, s1, __ldg(ks + i), p.L, p.LM, p.RM);
+#else
+    const uint32_t* ks = p.gkeys ? p.gkeys : p.keys;
+    for (int i = 0; i < p.rounds; ++i) philox_round<D>(s0, s1, ks[i], p.L, p.LM, p.RM);
+#endif
+  }
+  return (static_cast<uint64_t>(s0) << p.R) | (s1 & p.RM);
+}
+
+template <int D, int NR>
+BSG_HD uint64_t philox_inv(uint64_t y, const BijParams& p) {
+  uint32_t t0 = static_cast<uint32_t>(y >> p.R);
+  uint32_t t1 = static_cast<uint32_t>(y) & p.RM;
+  if constexpr (NR > 0) {
+#pragma unroll
+    for (int i = NR - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, p.keys[i], p.L, p.LM);
+  } else {
+#ifdef __CUDA_ARCH__
+    const uint32_t* ks = p.gkeys;
+    for (int i = p.rounds - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, __ldg(ks + i), p.L, p.LM);
+#else
+    const uint32_t* ks = p.gkeys ? p.gkeys : p.keys;
+    for (int i = p.rounds - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, ks[i], p.L, p.LM);
+#endif
+  }
+  return (static_cast<uint64_t>(t0) << p.R) | (t1 & p.RM);
+}
+
+// 32-bit-counter specialisations (bits <= 32): identical arithmetic, no
+// 64-bit shifts in the kernel's address path.
+template <int D, int NR>
+BSG_HD uint32_t philox_fwd32(uint32_t x, const BijParams& p) {
+  uint32_t s0 = x >> p.R;
+  uint32_t s1 = x & p.RM;
+#pragma unroll
+  for (int i = 0; i < NR; ++i) philox_round<D>(s0, s1, p.keys[i], p.L, p.LM, p.RM);
+  return (s0 << p.R) | (s1 & p.RM);
+}
+
+// LCG (shuffle.hpp:160-162): (a*x + c) mod 2^64, masked to the domain.
+BSG_HD uint64_t lcg_fwd(uint64_t x, const BijParams& p) { return (p.lcg_a * x + p.lcg_c) & p.mask; }
+BSG_HD uint64_t lcg_inv(uint64_t y, const BijParams& p) { return (p.lcg_ainv * (y - p.lcg_c)) & p.mask; }
+BSG_HD uint32_t lcg_fwd32(uint32_t x, const BijParams& p) {
+  return (static_cast<uint32_t>(p.lcg_a) * x + static_cast<uint32_t>(p.lcg_c)) & static_cast<uint32_t>(p.mask);
+}
+
+// Host-side construction of BijParams; mirrors make_lcg / make_philox
+// (bijection.hpp:25-34, 73-88) including their argument checks.
+// Returns 0 on success, 1 (invalid argument) on a reference-rejected input.
+inline int make_params(int variant, int bits, uint64_t seed, int rounds, BijParams& p) {
+  p = BijParams{};
+  p.variant = variant;
+  p.bits = bits;
+  if (variant == kLcg) {
+    if (bits < 1 || bits > 63) return 1;  // bijection.hpp:26-27
+    p.mask = (1ULL << bits) - 1;
+    p.lcg_a = (mix64(seed) | 1ULL) & p.mask;
+    p.lcg_c = mix64(seed + 1) & p.mask;
+    p.lcg_ainv = odd_inverse_pow2_64(p.lcg_a);
+    p.rounds = rounds;
+    return 0;
+  }
+  if (bits < 2 || bits > 63) return 1;  // bijection.hpp:75-76
+  if (rounds < 3) return 1;             // bijection.hpp:77-78
+  p.mask = (1ULL << bits) - 1;
+  p.L = bits / 2;
+  p.R = bits - p.L;
+  p.LM = static_cast<uint32_t>((1ULL << p.L) - 1);
+  p.RM = static_cast<uint32_t>((1ULL << p.R) - 1);
+  p.rounds = rounds;
+  for (int i = 0; i < rounds && i < kParamKeys; ++i) p.keys[i] = round_key(seed, i);
+  return 0;
+}
+
+// Host scalar evaluation (any rounds; keys regenerated on the fly when the
+// schedule is longer than the parameter block).
+inline uint64_t host_apply(const BijParams& p, uint64_t seed, uint64_t x, bool inverse) {
+  if (p.variant == kLcg) return inverse ? lcg_inv(x, p) : lcg_fwd(x, p);
+  const int L = p.L, R = p.R, d = R - L;
+  uint32_t a = static_cast<uint32_t>(x >> R), b = static_cast<uint32_t>(x) & p.RM;
+  auto key = [&](int i) { return i < kParamKeys ? p.keys[i] : round_key(seed, i); };
+  if (!inverse) {
+    for (int i = 0; i < p.rounds; ++i) {
+      if (d) philox_round<1>(a, b, key(i), L, p.LM, p.RM);
+      else philox_round<0>(a, b, key(i), L, p.LM, p.RM);
+    }
+  } else {
+    for (int i = p.rounds - 1; i >= 0; --i) {
+      if (d) philox_inv_round<1>(a, b, key(i), L, p.LM);
+      else philox_inv_round<0>(a, b, key(i), L, p.LM);
+    }
+  }
+  return (static_cast<uint64_t>(a) << R) | (b & p.RM);
+}
+
+}  // namespace bsg

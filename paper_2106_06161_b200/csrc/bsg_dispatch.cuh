@@ -1,0 +1,105 @@
+// bsg_dispatch.cuh -- template dispatch from a ShuffleLaunch to a concrete
+// kernel instantiation.  Included by one translation unit per payload type
+// (bsg_k_*.cu) so the instantiations compile in parallel.
+#pragma once
+
+#include <type_traits>
+
+#include "bsg_kernels.cuh"
+#include "bsg_payload.h"
+
+namespace bsg {
+
+template <int KIND, typename CT, typename T, bool SH>
+cudaError_t run_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
+  const uint64_t len = a.c1 - a.c0;
+  if (len == 0) return cudaSuccess;
+  if (!a.compact) {
+    constexpr uint64_t kTile = kThreads * kPow2Items;
+    const uint64_t grid = (len + kTile - 1) / kTile;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    k_pow2<KIND, CT, T, SH, kPow2Items><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a.src, a.out, a.c0, a.c1,
+                                                                                         a.p);
+  } else {
+    constexpr uint64_t kTile = kThreads * kCompactItems;
+    const uint64_t grid = (len + kTile - 1) / kTile;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    k_compact<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+        a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int KIND, typename CT, typename T>
+cudaError_t run_sh(const ShuffleLaunch& a, cudaStream_t s) {
+  if constexpr (!std::is_same<T, IdxTag>::value) {
+    if (a.src.nshards > 0) return run_shuffle<KIND, CT, T, true>(a, s);
+  }
+  return run_shuffle<KIND, CT, T, false>(a, s);
+}
+
+template <typename T>
+cudaError_t dispatch_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
+  const bool narrow = a.p.bits <= 32;
+  switch (kind_of(a.p)) {
+    case kKindLcg:
+      return narrow ? run_sh<kKindLcg, uint32_t, T>(a, s) : run_sh<kKindLcg, uint64_t, T>(a, s);
+    case kKindPh0:
+      return narrow ? run_sh<kKindPh0, uint32_t, T>(a, s) : run_sh<kKindPh0, uint64_t, T>(a, s);
+    case kKindPh1:
+      return narrow ? run_sh<kKindPh1, uint32_t, T>(a, s) : run_sh<kKindPh1, uint64_t, T>(a, s);
+    case kKindPh0G:
+      return run_sh<kKindPh0G, uint64_t, T>(a, s);
+    case kKindPh1G:
+      return run_sh<kKindPh1G, uint64_t, T>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int KIND, typename T>
+cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(a.m) * sizeof(T);
+  auto kern = k_batched<KIND, T>;
+  static thread_local size_t configured = 0;  // per instantiation: raised opt-in limit
+  if (smem > 48 * 1024 && configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (per_sm < 1) return cudaErrorNotSupported;
+  const uint64_t want = static_cast<uint64_t>(sms) * per_sm;
+  const unsigned grid = static_cast<unsigned>(a.batch < want ? a.batch : want);
+  kern<<<grid, kThreads, smem, s>>>(static_cast<const T*>(a.in), static_cast<T*>(a.out), a.batch, a.m, a.seed, a.p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch_batched(const BatchedLaunch& a, cudaStream_t s) {
+  switch (kind_of(a.p)) {
+    case kKindLcg: return run_batched<kKindLcg, T>(a, s);
+    case kKindPh0: return run_batched<kKindPh0, T>(a, s);
+    case kKindPh1: return run_batched<kKindPh1, T>(a, s);
+    case kKindPh0G: return run_batched<kKindPh0G, T>(a, s);
+    case kKindPh1G: return run_batched<kKindPh1G, T>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t dispatch_gather(const void* src, const uint64_t* idx, void* out, uint64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  constexpr uint64_t kTile = kThreads * 8;
+  const uint64_t grid = (n + kTile - 1) / kTile;
+  k_gather<T, 8><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(static_cast<const T*>(src), idx,
+                                                                   static_cast<T*>(out), n);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace bsg

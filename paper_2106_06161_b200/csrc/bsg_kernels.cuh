@@ -1,0 +1,398 @@
+// bsg_kernels.cuh -- sm_100a kernels of the bijective shuffle.
+//
+// Hot path (the paper's Bijective2 design, rebuilt for
+// B200): ONE kernel per shuffle that
+//   1. evaluates the keyed bijection on a tile of counters (registers only),
+//   2. flags images < m and ranks them in counter order with warp ballots and
+//      a shared-memory scan,
+//   3. issues the payload loads in[image] immediately (their DRAM latency
+//      overlaps the scan and the look-back),
+//   4. resolves the tile's output offset with a decoupled look-back over
+//      dynamically numbered tiles,
+//   5. writes the payload at out[offset + rank] (each warp's survivors of one
+//      item form one contiguous run, so stores coalesce).
+// Every element therefore costs one read and one write of HBM.  When every
+// image survives (m == 2^bits) steps 2-4 vanish: out[c] = in[f(c)].
+//
+// Reference equivalents: chained_compact + philox_compact_avx512 +
+// ValuesSink (proj/include/bijshuf/shuffle.hpp:107-147, 193-212;
+// simd.hpp:72-131).  Output is independent of tile geometry, as the
+// reference's is of chunking (shuffle.hpp:22-24).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "bsg_internal.h"
+
+namespace bsg {
+
+constexpr int kWarps = kThreads / 32;
+
+// ------------------------------------------------------------------ bijection
+template <int KIND, typename CT>
+__device__ __forceinline__ CT bij(CT x, const BijParams& p) {
+  if constexpr (KIND == kKindLcg) {
+    if constexpr (sizeof(CT) == 4) return lcg_fwd32(x, p);
+    else return lcg_fwd(x, p);
+  } else if constexpr (KIND == kKindPh0 || KIND == kKindPh1) {
+    constexpr int D = KIND == kKindPh1 ? 1 : 0;
+    if constexpr (sizeof(CT) == 4) return philox_fwd32<D, 24>(x, p);
+    else return philox_fwd<D, 24>(x, p);
+  } else {
+    constexpr int D = KIND == kKindPh1G ? 1 : 0;
+    return static_cast<CT>(philox_fwd<D, 0>(x, p));
+  }
+}
+
+// ------------------------------------------------------------- memory helpers
+// Random payload reads: non-coherent path, no L1 allocation (no reuse).
+template <typename T>
+__device__ __forceinline__ T ld_rand(const T* p);
+template <>
+__device__ __forceinline__ uint8_t ld_rand<uint8_t>(const uint8_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint8_t>(v);
+}
+template <>
+__device__ __forceinline__ uint16_t ld_rand<uint16_t>(const uint16_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+template <>
+__device__ __forceinline__ uint32_t ld_rand<uint32_t>(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+template <>
+__device__ __forceinline__ uint64_t ld_rand<uint64_t>(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 ld_rand<uint4>(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Output stores: streaming (evict-first); the output is never re-read here.
+template <typename T>
+__device__ __forceinline__ void st_out(T* p, const T& v) {
+  __stcs(p, v);
+}
+template <>
+__device__ __forceinline__ void st_out<uint8_t>(uint8_t* p, const uint8_t& v) {
+  asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "h"(static_cast<unsigned short>(v)));
+}
+template <>
+__device__ __forceinline__ void st_out<uint16_t>(uint16_t* p, const uint16_t& v) {
+  asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v));
+}
+template <>
+__device__ __forceinline__ void st_out<uint32_t>(uint32_t* p, const uint32_t& v) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+template <>
+__device__ __forceinline__ void st_out<uint64_t>(uint64_t* p, const uint64_t& v) {
+  asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
+template <typename T, bool SH>
+__device__ __forceinline__ T load_src(const Src& s, uint64_t y) {
+  if constexpr (!SH) {
+    return ld_rand(static_cast<const T*>(s.base) + y);
+  } else {
+    uint64_t g, off;
+    if (s.shard_shift >= 0) {
+      g = y >> s.shard_shift;
+      off = y & (s.shard_elems - 1);
+    } else {
+      g = y / s.shard_elems;
+      off = y - g * s.shard_elems;
+    }
+    return ld_rand(static_cast<const T*>(s.shard[g]) + off);
+  }
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ----------------------------------------------------------------- pow2 path
+// m == 2^bits: every image survives, out[c - c0] = in[f(c)].
+template <int KIND, typename CT, typename T, bool SH, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_pow2(Src src, void* out_, uint64_t c0, uint64_t c1, BijParams p) {
+  constexpr int kTile = kThreads * ITEMS;
+  const uint64_t t0 = c0 + static_cast<uint64_t>(blockIdx.x) * kTile + threadIdx.x;
+  const bool full = c0 + (static_cast<uint64_t>(blockIdx.x) + 1) * kTile <= c1;
+  CT img[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) img[j] = bij<KIND, CT>(static_cast<CT>(t0 + j * kThreads), p);
+  if constexpr (std::is_same<T, IdxTag>::value) {
+    uint64_t* out = static_cast<uint64_t*>(out_) + (t0 - c0);
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if (full || t0 + j * kThreads < c1) st_out<uint64_t>(out + j * kThreads, static_cast<uint64_t>(img[j]));
+  } else {
+    T v[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if (full || t0 + j * kThreads < c1) v[j] = load_src<T, SH>(src, img[j]);
+    T* out = static_cast<T*>(out_) + (t0 - c0);
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if (full || t0 + j * kThreads < c1) st_out<T>(out + j * kThreads, v[j]);
+  }
+}
+
+// ------------------------------------------------------------ compacting path
+constexpr unsigned long long kFlagAgg = 1ULL << 62;
+constexpr unsigned long long kFlagPre = 2ULL << 62;
+constexpr unsigned long long kValMask = (1ULL << 40) - 1;
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, uint32_t epoch,
+                                                          unsigned long long v) {
+  return flag | (static_cast<unsigned long long>(epoch & 0x3FFFFFu) << 40) | (v & kValMask);
+}
+
+// Warp 0: publish this tile's aggregate, walk back over predecessors 32 at a
+// time until an inclusive prefix is found, publish the inclusive prefix and
+// return the exclusive prefix (CUB-style decoupled look-back).
+__device__ __forceinline__ unsigned long long lookback_warp(const Lookback& lb, uint32_t tile,
+                                                            unsigned long long total) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long* st = lb.status;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed_gpu(st, pack_status(kFlagPre, lb.epoch, total));
+    return 0;
+  }
+  if (lane == 0) st_relaxed_gpu(st + tile, pack_status(kFlagAgg, lb.epoch, total));
+  const uint32_t ep = lb.epoch & 0x3FFFFFu;
+  unsigned long long excl = 0;
+  long long base = static_cast<long long>(tile) - 1;
+  for (;;) {
+    const long long idx = base - lane;
+    unsigned long long w = 0;
+    unsigned flag = 2;  // lanes past tile 0 behave as an inclusive zero
+    if (idx >= 0) {
+      int spins = 0;
+      for (;;) {
+        w = ld_relaxed_gpu(st + idx);
+        flag = static_cast<unsigned>(w >> 62);
+        if (flag != 0 && static_cast<uint32_t>((w >> 40) & 0x3FFFFFu) == ep) break;
+        if (++spins > 8) __nanosleep(64);
+      }
+    }
+    const unsigned pmask = __ballot_sync(0xFFFFFFFFu, flag == 2);
+    const int k = pmask ? __ffs(pmask) - 1 : 31;
+    unsigned long long v = (lane <= k && idx >= 0) ? (w & kValMask) : 0ULL;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    excl += v;
+    if (pmask) break;
+    base -= 32;
+  }
+  if (lane == 0) st_relaxed_gpu(st + tile, pack_status(kFlagPre, lb.epoch, excl + total));
+  return excl;
+}
+
+template <int KIND, typename CT, typename T, bool SH, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_compact(Src src, void* out_, uint64_t m, uint64_t c0, uint64_t c1,
+                                                      BijParams p, Lookback lb, unsigned long long* count_out) {
+  constexpr int kTile = kThreads * ITEMS;
+  constexpr int kSlots = ITEMS * kWarps;       // (item, warp) counts in counter order
+  constexpr int kPerLane = kSlots / 32;
+  static_assert(kSlots % 32 == 0, "slots");
+  __shared__ uint32_t s_cnt[kSlots];
+  __shared__ unsigned long long s_prefix, s_total;
+  __shared__ uint32_t s_tile;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(lb.tile_counter, 1u);
+    if (t == gridDim.x - 1) *lb.tile_counter = 0;  // last ticket: reset for the next launch
+    s_tile = t;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = c0 + static_cast<uint64_t>(tile) * kTile + tid;
+
+  CT img[ITEMS];
+  uint32_t mask[ITEMS];
+  using V = typename std::conditional<std::is_same<T, IdxTag>::value, uint64_t, T>::type;
+  V v[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint64_t c = t0 + j * kThreads;
+    img[j] = bij<KIND, CT>(static_cast<CT>(c), p);
+    const bool keep = (c < c1) && (static_cast<uint64_t>(img[j]) < m);
+    mask[j] = __ballot_sync(0xFFFFFFFFu, keep);
+    if constexpr (!std::is_same<T, IdxTag>::value) {
+      if (keep) v[j] = load_src<T, SH>(src, img[j]);  // in flight during scan + look-back
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) s_cnt[j * kWarps + warp] = __popc(mask[j]);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t a[kPerLane], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kPerLane; ++i) {
+      a[i] = s_cnt[lane * kPerLane + i];
+      sum += a[i];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int i = 0; i < kPerLane; ++i) {
+      s_cnt[lane * kPerLane + i] = run;  // exclusive, in place
+      run += a[i];
+    }
+    const unsigned long long total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    const unsigned long long excl = lookback_warp(lb, tile, total);
+    if (lane == 0) {
+      s_prefix = excl;
+      s_total = total;
+    }
+  }
+  __syncthreads();
+  const unsigned long long prefix = s_prefix;
+  const uint32_t lt = lanemask_lt();
+  V* out = static_cast<V*>(out_);
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    if ((mask[j] >> lane) & 1u) {
+      const uint64_t pos = prefix + s_cnt[j * kWarps + warp] + __popc(mask[j] & lt);
+      if constexpr (std::is_same<T, IdxTag>::value) st_out<uint64_t>(out + pos, static_cast<uint64_t>(img[j]));
+      else st_out<T>(out + pos, v[j]);
+    }
+  }
+  if (count_out != nullptr && tile == gridDim.x - 1 && tid == 0) *count_out = prefix + s_total;
+}
+
+// --------------------------------------------------------------- batched path
+// Many independent shuffles of the same length m (BijectiveShuffleSampler,
+// stats.hpp:314-324: shuffle b is keyed by seed + b).  One CTA per shuffle:
+// the row is staged in shared memory, round keys are derived on device, the
+// cipher runs from registers and the payload is gathered from shared memory,
+// so HBM sees one coalesced read and one coalesced write per element.
+template <int D, int NR>
+__device__ __forceinline__ uint32_t philox_keys_fwd(uint32_t x, const uint32_t* k, int L, int R, uint32_t LM,
+                                                    uint32_t RM, int rounds) {
+  uint32_t s0 = x >> R, s1 = x & RM;
+  if constexpr (NR > 0) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) philox_round<D>(s0, s1, k[i], L, LM, RM);
+  } else {
+    for (int i = 0; i < rounds; ++i) philox_round<D>(s0, s1, k[i], L, LM, RM);
+  }
+  return (s0 << R) | (s1 & RM);
+}
+
+template <int KIND, typename T>
+__global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, T* __restrict__ out, uint64_t batch,
+                                                      uint32_t m, uint64_t seed, BijParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s_row = reinterpret_cast<T*>(smem_raw);
+  __shared__ uint32_t s_keys[kBatchedMaxRounds];
+  __shared__ uint32_t s_wcnt[2][kWarps];
+  constexpr bool kFast = (KIND == kKindPh0 || KIND == kKindPh1);
+  constexpr int D = (KIND == kKindPh1 || KIND == kKindPh1G) ? 1 : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = 1u << p.bits;
+  const uint32_t mask32 = n - 1;
+  const bool pow2 = (m == n);
+  for (uint64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const uint64_t sb = seed + b;
+    if (KIND != kKindLcg && tid < p.rounds) s_keys[tid] = round_key(sb, tid);
+    const T* row_in = in + b * m;
+    T* row_out = out + b * m;
+    for (uint32_t i = tid; i < m; i += kThreads) s_row[i] = row_in[i];
+    __syncthreads();
+    uint32_t kr[kFast ? 24 : 1];
+    if constexpr (kFast) {
+#pragma unroll
+      for (int i = 0; i < 24; ++i) kr[i] = s_keys[i];
+    }
+    // LCG parameters of this shuffle (make_lcg, bijection.hpp:25-34)
+    const uint32_t la = static_cast<uint32_t>((mix64(sb) | 1ULL)) & mask32;
+    const uint32_t lc = static_cast<uint32_t>(mix64(sb + 1)) & mask32;
+    auto f = [&](uint32_t c) -> uint32_t {
+      if constexpr (KIND == kKindLcg) return (la * c + lc) & mask32;
+      else if constexpr (kFast) return philox_keys_fwd<D, 24>(c, kr, p.L, p.R, p.LM, p.RM, 24);
+      else return philox_keys_fwd<D, 0>(c, s_keys, p.L, p.R, p.LM, p.RM, p.rounds);
+    };
+    if (pow2) {
+      for (uint32_t c = tid; c < n; c += kThreads) st_out<T>(row_out + c, s_row[f(c)]);
+    } else {
+      uint32_t base = 0;
+      int buf = 0;
+      for (uint32_t c0 = 0; c0 < n; c0 += kThreads) {
+        const uint32_t c = c0 + tid;
+        const uint32_t y = f(c);
+        const bool keep = y < m;  // c < n always (n is a multiple of 256 or the loop is single)
+        const uint32_t bm = __ballot_sync(0xFFFFFFFFu, keep && c < n);
+        if (lane == 0) s_wcnt[buf][warp] = __popc(bm);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const uint32_t x = s_wcnt[buf][w];
+          before += (w < warp) ? x : 0;
+          total += x;
+        }
+        if (keep && c < n) st_out<T>(row_out + base + before + __popc(bm & lanemask_lt()), s_row[y]);
+        base += total;
+        buf ^= 1;  // double-buffered counts: one barrier per chunk
+      }
+    }
+    __syncthreads();  // s_row / s_keys reuse by the next shuffle
+  }
+}
+
+// --------------------------------------------------------------------- gather
+// out[i] = src[idx[i]] (shuffle.hpp:319-334, the paper's "Gather" bound).
+template <typename T, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_gather(const T* __restrict__ src, const uint64_t* __restrict__ idx,
+                                                     T* __restrict__ out, uint64_t n) {
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kThreads * ITEMS + threadIdx.x;
+  uint64_t ix[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint64_t i = t0 + j * kThreads;
+    ix[j] = i < n ? __ldcs(idx + i) : 0;
+  }
+  T v[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j)
+    if (t0 + j * kThreads < n) v[j] = ld_rand(src + ix[j]);
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j)
+    if (t0 + j * kThreads < n) st_out<T>(out + t0 + j * kThreads, v[j]);
+}
+
+}  // namespace bsg

@@ -1,0 +1,377 @@
+"""GPU parity: the sm_100a kernels through the C ABI against the oracle and the
+reference-generated fixtures.  Bit-exact throughout (integer/index work)."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+PHILOX, LCG = O.PHILOX, O.LCG
+
+
+def cfg_of(bsg, seed=0, variant=PHILOX, rounds=24, workers=0):
+    return bsg.ShuffleConfig(seed=seed, variant=bsg.BijectionVariant(variant), num_rounds=rounds, workers=workers)
+
+
+def gpu_indices(bsg, cuda, m, **kw):
+    t = bsg.shuffle_indices(m, cfg_of(bsg, **kw), device="cuda")
+    return t.cpu().numpy().view(np.uint64)
+
+
+# ------------------------------------------------------------ bijections --
+def test_bijection_apply_matches_fixtures(bsg, cuda, golden):
+    by = {}
+    for bits, seed, rounds, x, y in golden["philox_apply"]:
+        by.setdefault((bits, seed, rounds), []).append((x, y))
+    for (bits, seed, rounds), xy in by.items():
+        xs = np.array([a for a, _ in xy], dtype=np.uint64)
+        ys = np.array([b for _, b in xy], dtype=np.uint64)
+        got = bsg.bijection_apply(bsg.BijectionVariant.VariablePhilox, bits, seed, rounds, xs)
+        assert np.array_equal(got, ys), (bits, seed, rounds)
+        back = bsg.bijection_apply(bsg.BijectionVariant.VariablePhilox, bits, seed, rounds, ys, inverse=True)
+        assert np.array_equal(back, xs), (bits, seed, rounds)
+
+
+def test_bijection_apply_exhaustive_widths(bsg, cuda):
+    for bits in range(2, 23):
+        for variant in (PHILOX, LCG):
+            n = 1 << bits
+            x = cuda.arange(n, dtype=cuda.int64, device="cuda")
+            y = bsg.bijection_apply(bsg.BijectionVariant(variant), bits, 0xABC + bits, 24, x)
+            yn = y.cpu().numpy().view(np.uint64)
+            assert np.array_equal(np.sort(yn), np.arange(n, dtype=np.uint64)), (bits, variant)
+            if variant == PHILOX:
+                idx = np.linspace(0, n - 1, 64).astype(np.uint64)
+                exp = [O.philox_apply(bits, 0xABC + bits, 24, int(i)) for i in idx]
+                assert np.array_equal(yn[idx.astype(np.int64)], np.array(exp, dtype=np.uint64))
+            inv = bsg.bijection_apply(bsg.BijectionVariant(variant), bits, 0xABC + bits, 24, y, inverse=True)
+            assert cuda.equal(inv, x)
+
+
+def test_bijection_apply_counter_mode_wide(bsg, cuda):
+    for bits in (33, 40, 47, 63):
+        start = (1 << bits) - 5000
+        y = bsg.bijection_apply(bsg.BijectionVariant.VariablePhilox, bits, 77, 24, None, start=start, n=5000)
+        exp = np.array([O.philox_apply(bits, 77, 24, start + i) for i in range(0, 5000, 97)], dtype=np.uint64)
+        assert np.array_equal(y[::97], exp)
+
+
+def test_bijection_apply_rejects_out_of_domain(bsg, cuda):
+    with pytest.raises(bsg.OutOfRange):
+        bsg.bijection_apply(bsg.BijectionVariant.VariablePhilox, 8, 7, 24, np.array([256], dtype=np.uint64))
+
+
+# -------------------------------------------------------------- indices --
+def test_indices_full_fixtures(bsg, cuda, golden):
+    for case in golden["indices_full"]:
+        got = gpu_indices(bsg, cuda, case["m"], seed=case["seed"], variant=case["variant"], rounds=case["rounds"])
+        assert [int(v) for v in got] == case["perm"], case["m"]
+
+
+def test_indices_hash_fixtures(bsg, cuda, golden):
+    for case in golden["indices_hash"]:
+        got = gpu_indices(bsg, cuda, case["m"], seed=case["seed"], variant=case["variant"], rounds=case["rounds"])
+        assert f"{O.fnv1a64(got):016x}" == case["fnv"], case
+        assert [int(v) for v in got[:8]] == case["head"]
+
+
+def test_indices_exhaustive_small_sizes(bsg, cuda):
+    for m in range(0, 2200):
+        for variant, seed in ((PHILOX, m * 31 + 1), (LCG, m)):
+            got = gpu_indices(bsg, cuda, m, seed=seed, variant=variant)
+            exp = O.shuffle_indices(m, seed, variant, 24)
+            assert np.array_equal(got, exp), (m, variant)
+
+
+def test_indices_pow2_boundaries(bsg, cuda):
+    for k in range(4, 25):
+        for m in ((1 << k) - 1, 1 << k, (1 << k) + 1):
+            for variant in (PHILOX, LCG):
+                got = gpu_indices(bsg, cuda, m, seed=k, variant=variant)
+                assert np.array_equal(got, O.shuffle_indices(m, k, variant, 24)), (m, variant)
+
+
+def test_generic_round_counts(bsg, cuda):
+    for rounds in (3, 4, 7, 12, 23, 25, 31, 32, 33, 64, 100):
+        for m in (1000, 4096, 70001):
+            got = gpu_indices(bsg, cuda, m, seed=rounds, rounds=rounds)
+            assert np.array_equal(got, O.shuffle_indices(m, rounds, PHILOX, rounds)), (m, rounds)
+
+
+def test_force_compact_equals_pow2_path(bsg, cuda):
+    for m in (16, 1 << 12, 1 << 20, 1 << 23):
+        base = gpu_indices(bsg, cuda, m, seed=3)
+        old = bsg.set_force_compact(True)
+        try:
+            comp = gpu_indices(bsg, cuda, m, seed=3)
+        finally:
+            bsg.set_force_compact(old)
+        assert np.array_equal(base, comp), m
+
+
+def test_host_pointer_path_and_workers(bsg, cuda):
+    m = (1 << 18) + 12345  # unit_shuffle.cpp:96-107
+    exp = O.shuffle_indices(m, 17)
+    for w in (1, 2, 8, 0):
+        got = bsg.shuffle_indices(m, cfg_of(bsg, seed=17, workers=w))  # numpy (host) output
+        assert np.array_equal(got, exp)
+
+
+def test_determinism_acceptance_case(bsg, cuda):  # acceptance.cpp:232-244
+    a = gpu_indices(bsg, cuda, 1000001, seed=7)
+    b = gpu_indices(bsg, cuda, 1000001, seed=7)
+    assert np.array_equal(a, b) and O.is_valid_permutation(a)
+    assert np.array_equal(a, O.shuffle_indices(1000001, 7))
+
+
+def test_invalid_arguments(bsg, cuda):
+    with pytest.raises(bsg.InvalidArgument):
+        bsg.shuffle_indices(100, cfg_of(bsg, rounds=2))
+    # m <= 2 never validates (shuffle.hpp:228-240)
+    assert list(bsg.shuffle_indices(2, cfg_of(bsg, rounds=0, seed=5))) == [O.C.orc_mix64(5) & 1,
+                                                                           (O.C.orc_mix64(5) & 1) ^ 1]
+    v = np.arange(10, dtype=np.uint64)
+    with pytest.raises(bsg.InvalidArgument):
+        bsg.shuffle_values_into(v, cfg_of(bsg), v)
+    t = cuda.arange(10, device="cuda")
+    with pytest.raises(bsg.InvalidArgument):
+        bsg.shuffle_values_into(t, cfg_of(bsg), t)
+
+
+# --------------------------------------------------------------- values --
+def _values_input(m, eb):
+    raw = (np.arange(m * eb, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)).astype(np.uint8)
+    return raw.reshape(m, eb)
+
+
+def _fnv_bytes(a):
+    b = np.ascontiguousarray(a).tobytes()
+    b += bytes((-len(b)) % 8)
+    return f"{O.fnv1a64(np.frombuffer(b, dtype=np.uint64)):016x}"
+
+
+def test_values_fixtures_all_element_sizes(bsg, cuda, golden):
+    for case in golden["values_hash"]:
+        raw = _values_input(case["m"], case["elem_bytes"])
+        eb = case["elem_bytes"]
+        dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}.get(eb)
+        if dt is not None:
+            arr = raw.view(dt).reshape(case["m"])
+        else:
+            arr = raw.view(np.dtype((np.void, eb))).reshape(case["m"])
+        cfg = cfg_of(bsg, seed=case["seed"], variant=case["variant"], rounds=case["rounds"])
+        out = bsg.shuffle_values(arr, cfg)  # host path
+        assert _fnv_bytes(out) == case["fnv_bytes"], case
+        if dt is not None or eb == 16:
+            td = cuda.from_numpy(raw.copy()).cuda()  # (m, eb) uint8 device tensor
+            if eb in (2, 4, 8):
+                td = td.view({2: cuda.int16, 4: cuda.int32, 8: cuda.int64}[eb]).reshape(case["m"])
+            elif eb == 16:
+                td = td.view(cuda.int64).reshape(case["m"], 2)
+            else:
+                td = td.reshape(case["m"])
+            od = cuda.empty_like(td)
+            bsg.shuffle_values_into(td, cfg, od) if eb != 16 else _values16(bsg, td, od, cfg)
+            cuda.cuda.synchronize()
+            assert _fnv_bytes(od.cpu().numpy()) == case["fnv_bytes"], case
+
+
+def _values16(bsg, td, od, cfg):
+    from paper_2106_06161_b200 import _lib
+    _lib.check(_lib.lib.bsg_shuffle_values(td.data_ptr(), od.data_ptr(), td.shape[0], 16,
+                                           ctypes.byref(cfg._c()), None), "values16")
+
+
+def test_values_match_indices(bsg, cuda):  # unit_shuffle.cpp:137-148
+    m = 70000
+    vals = cuda.arange(m, dtype=cuda.int64, device="cuda") * 3 + 1
+    out = bsg.shuffle_values(vals, cfg_of(bsg, seed=31))
+    perm = bsg.shuffle_indices(m, cfg_of(bsg, seed=31), device="cuda")
+    assert cuda.equal(out, vals[perm])
+
+
+def test_values_into_reuse_and_trivial(bsg, cuda):  # unit_shuffle.cpp:205-221
+    for m in (1000, 70000, 17, 2, 1, 0):
+        vals = (np.arange(m, dtype=np.uint64) * 7 + 3)
+        out = bsg.shuffle_values(vals, cfg_of(bsg, seed=21))
+        assert np.array_equal(out, O.shuffle_values(vals, 21)) if m else len(out) == 0
+
+
+def test_values_full_size_hashes(bsg, cuda, golden):
+    """The bench workload itself (2^29 u64) and the worst-case padding sizes, vs the reference run."""
+    for case in golden["values_full_hash"]:
+        m = case["m"]
+        vals = cuda.arange(m, dtype=cuda.int64, device="cuda")
+        out = bsg.shuffle_values(vals, cfg_of(bsg, seed=case["seed"], variant=case["variant"],
+                                              rounds=case["rounds"]))
+        host = out.cpu().numpy().view(np.uint64)
+        del vals, out
+        assert f"{O.fnv1a64(host):016x}" == case["fnv"], case
+        cuda.cuda.empty_cache()
+
+
+# --------------------------------------------------------------- ranges --
+def test_range_concatenation(bsg, cuda):
+    from paper_2106_06161_b200 import _lib
+    for m, variant in ((5000, PHILOX), ((1 << 20) + 3, PHILOX), ((1 << 20) + 3, LCG), (1 << 16, PHILOX)):
+        cfg = cfg_of(bsg, seed=9, variant=variant)._c()
+        n = 1 << O.C.orc_domain_bits(m)
+        cuts = [0, 1, 777, 4096, 4097, n // 2 + 13, n]
+        pieces = []
+        for a, b in zip(cuts, cuts[1:]):
+            out = cuda.empty(max(b - a, 1), dtype=cuda.int64, device="cuda")
+            cnt = ctypes.c_uint64()
+            _lib.check(_lib.lib.bsg_shuffle_range(m, ctypes.byref(cfg), a, b, None, None, out.data_ptr(), 8,
+                                                  ctypes.addressof(cnt), None), "range")
+            c2 = ctypes.c_uint64()
+            _lib.check(_lib.lib.bsg_range_count(m, ctypes.byref(cfg), a, b, ctypes.byref(c2), None), "count")
+            assert cnt.value == c2.value
+            pieces.append(out[:cnt.value].cpu().numpy().view(np.uint64))
+        assert np.array_equal(np.concatenate(pieces), O.shuffle_indices(m, 9, variant, 24)), m
+
+
+def test_wide_domain_ranges(bsg, cuda):
+    """bits > 32 (64-bit counters): indices and u8 payload on slices of the 2^33 domain."""
+    from paper_2106_06161_b200 import _lib
+    m = (1 << 32) + 5
+    cfg = cfg_of(bsg, seed=0x5EED)._c()
+    payload = (cuda.arange(m, dtype=cuda.int64, device="cuda") % 251).to(cuda.uint8)
+    for a, b in (((1 << 32) - 3000, (1 << 32) + 5000), (0, 6000), ((1 << 33) - 4096, 1 << 33)):
+        exp = O.shuffle_indices_range(m, 0x5EED, PHILOX, 24, a, b)
+        out = cuda.empty(b - a, dtype=cuda.int64, device="cuda")
+        cnt = ctypes.c_uint64()
+        _lib.check(_lib.lib.bsg_shuffle_range(m, ctypes.byref(cfg), a, b, None, None, out.data_ptr(), 8,
+                                              ctypes.addressof(cnt), None), "range")
+        assert cnt.value == len(exp)
+        assert np.array_equal(out[:cnt.value].cpu().numpy().view(np.uint64), exp)
+        outv = cuda.empty(b - a, dtype=cuda.uint8, device="cuda")
+        _lib.check(_lib.lib.bsg_shuffle_range(m, ctypes.byref(cfg), a, b, payload.data_ptr(), None,
+                                              outv.data_ptr(), 1, ctypes.addressof(cnt), None), "range u8")
+        assert np.array_equal(outv[:cnt.value].cpu().numpy(), (exp % 251).astype(np.uint8))
+    del payload
+    cuda.cuda.empty_cache()
+
+
+def test_sharded_input_equals_contiguous(bsg, cuda):
+    from paper_2106_06161_b200 import _lib
+    m, G = (1 << 20) + 777, 4
+    S = (m + G - 1) // G
+    vals = cuda.arange(G * S, dtype=cuda.int64, device="cuda") * 5 + 2
+    shards = [vals[g * S:(g + 1) * S].clone() for g in range(G)]
+    sh = _lib.bsg_shards()
+    for g in range(G):
+        sh.ptrs[g] = shards[g].data_ptr()
+    sh.count, sh.shard_elems = G, S
+    cfg = cfg_of(bsg, seed=4)._c()
+    n = 1 << O.C.orc_domain_bits(m)
+    out = cuda.empty(m, dtype=cuda.int64, device="cuda")
+    cnt = ctypes.c_uint64()
+    _lib.check(_lib.lib.bsg_shuffle_range(m, ctypes.byref(cfg), 0, n, None, ctypes.byref(sh), out.data_ptr(), 8,
+                                          ctypes.addressof(cnt), None), "sharded")
+    assert cnt.value == m
+    exp = bsg.shuffle_values(vals[:m].contiguous(), cfg_of(bsg, seed=4))
+    assert cuda.equal(out, exp)
+
+
+def test_dist_shuffle_single_process_ranks(bsg, cuda):
+    """Every rank of a simulated world, with the allgather answered from the count pass."""
+    from paper_2106_06161_b200 import _lib
+    m, W = (1 << 19) + 9, 3
+    cfg = cfg_of(bsg, seed=12)._c()
+    counts = []
+    for r in range(W):
+        b, e = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(_lib.lib.bsg_dist_counter_range(m, r, W, ctypes.byref(b), ctypes.byref(e)), "range")
+        c = ctypes.c_uint64()
+        _lib.check(_lib.lib.bsg_range_count(m, ctypes.byref(cfg), b.value, e.value, ctypes.byref(c), None), "cnt")
+        counts.append(c.value)
+
+    @_lib.ALLGATHER_FN
+    def ag(send, recv, user):
+        for i, c in enumerate(counts):
+            recv[i] = c
+        return 0
+
+    vals = cuda.arange(m, dtype=cuda.int64, device="cuda")
+    full = cuda.empty(m, dtype=cuda.int64, device="cuda")
+    for r in range(W):
+        out = cuda.empty(m, dtype=cuda.int64, device="cuda")
+        off, cnt = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(_lib.lib.bsg_dist_shuffle_values(m, ctypes.byref(cfg), r, W, vals.data_ptr(), None,
+                                                    out.data_ptr(), 8, ag, None, ctypes.byref(off),
+                                                    ctypes.byref(cnt), None), "dist")
+        assert cnt.value == counts[r]
+        full[off.value:off.value + cnt.value] = out[:cnt.value]
+    assert np.array_equal(full.cpu().numpy().view(np.uint64), O.shuffle_indices(m, 12))
+
+
+# ------------------------------------------------------------- batched --
+def test_batched_fixtures(bsg, cuda, golden):
+    for case in golden["batched"]:
+        m = case["m"]
+        batch = 4
+        vals = cuda.arange(m, dtype=cuda.int32, device="cuda").repeat(batch, 1)
+        out = bsg.shuffle_values_batched(vals, cfg_of(bsg, seed=case["seed"], variant=case["variant"],
+                                                      rounds=case["rounds"]))
+        for row in case["rows"]:
+            got = out[row["b"]].cpu().numpy().astype(np.uint64)
+            assert f"{O.fnv1a64(got):016x}" == row["fnv"], (m, row["b"])
+
+
+def test_batched_vs_oracle_many(bsg, cuda):
+    rng = np.random.default_rng(3)
+    for m, dt, rounds, variant in ((1024, np.uint32, 24, PHILOX), (1000, np.uint64, 24, PHILOX),
+                                   (4096, np.uint16, 24, LCG), (3, np.uint8, 24, PHILOX), (777, np.uint32, 12, PHILOX),
+                                   (1 << 14, np.uint64, 24, PHILOX), (5000, np.uint32, 31, PHILOX),
+                                   (2, np.uint32, 24, PHILOX), (1 << 17, np.uint32, 24, PHILOX)):
+        batch = 37
+        vals = rng.integers(0, np.iinfo(dt).max, size=(batch, m), dtype=dt)
+        got = bsg.shuffle_values_batched(vals, cfg_of(bsg, seed=123, variant=variant, rounds=rounds))
+        exp = O.shuffle_values_batched(vals, 123, variant, rounds)
+        assert np.array_equal(got, exp), (m, dt, rounds)
+
+
+def test_batched_c4_shape(bsg, cuda):
+    """C4: 65536 shuffles of 1024 u32 (one GPU's share of 8192 checked against the oracle)."""
+    batch, m = 8192, 1024
+    vals = cuda.randint(0, 2**31 - 1, (batch, m), dtype=cuda.int32, device="cuda")
+    out = bsg.shuffle_values_batched(vals, cfg_of(bsg, seed=1000))
+    vh, oh = vals.cpu().numpy().view(np.uint32), out.cpu().numpy().view(np.uint32)
+    for b in (0, 1, 2, 4095, 8191):
+        perm = O.shuffle_indices(m, 1000 + b)
+        assert np.array_equal(oh[b], vh[b][perm.astype(np.int64)])
+
+
+# --------------------------------------------------------------- gather --
+def test_gather(bsg, cuda):  # unit_shuffle.cpp:422-442
+    src = np.array([10, 20, 30], dtype=np.uint64)
+    idx = np.array([2, 2, 0, 1], dtype=np.uint64)
+    assert list(bsg.gather(src, idx)) == [30, 30, 10, 20]
+    with pytest.raises(bsg.InvalidArgument):
+        bsg.gather_into(src, idx, src)
+    big = cuda.arange(1 << 22, dtype=cuda.int64, device="cuda") * 3
+    ix = cuda.randint(0, 1 << 22, (1 << 21,), device="cuda")
+    assert cuda.equal(bsg.gather(big, ix), big[ix])
+    for dt in (cuda.uint8, cuda.int16, cuda.int32):
+        s = (cuda.arange(1000, device="cuda") % 100).to(dt)
+        i = cuda.randint(0, 1000, (5000,), device="cuda")
+        assert cuda.equal(bsg.gather(s, i), s[i])
+
+
+def test_sort_shuffle_baseline_is_permutation(bsg, cuda):
+    n = 1 << 20
+    v = cuda.arange(n, dtype=cuda.int64, device="cuda")
+    out = bsg.sort_shuffle_u64(v, 1)
+    assert cuda.equal(out.sort().values, v) and not cuda.equal(out, v)
+
+
+def test_kernel_launch_counter_moves(bsg, cuda):
+    before = bsg.kernel_launches()
+    bsg.shuffle_indices(1 << 20, cfg_of(bsg), device="cuda")
+    cuda.cuda.synchronize()
+    assert bsg.kernel_launches() > before
