@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the bijective shuffle hot path (BASELINE.json north star).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c1|c4]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+A step = one full shuffle of the configured workload.  `value` is the
+whole-job effective bandwidth 2*n*elem_bytes / time with inputs resident in
+HBM (CUDA events on the launching stream, max over ranks); `e2e` is the same
+metric through the public API with pinned HOST buffers (H2D + shuffle + D2H
+every step).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "effective shuffle GB/s (2·n·bytes/time) vs HBM peak, n=2^29 u64, 1/2/4/8 B200"
+SEED = 0x5EED
+
+CONFIGS = {
+    # name: (m per GPU, elem bytes, variant, batch, description)
+    "c2": (1 << 29, 8, 1, 0, "C2: n=2^29 uint64, power-of-two domain, VariablePhilox-24"),
+    "c3": ((1 << 29) + 1, 8, 1, 0, "C3: n=2^29+1 uint64, worst-case padding (2^30 counters), VariablePhilox-24"),
+    "c3lcg": ((1 << 29) + 1, 8, 0, 0, "C3: n=2^29+1 uint64, worst-case padding (2^30 counters), LCG"),
+    "c2lcg": (1 << 29, 8, 0, 0, "C2: n=2^29 uint64, power-of-two domain, LCG"),
+    "c1": (1 << 20, 8, 1, 0, "C1: n=2^20 uint64, VariablePhilox-24"),
+    "c4": (1024, 4, 1, 8192, "C4: 8192 shuffles of n=1024 uint32 per GPU (65536 over 8), VariablePhilox-24"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--no-comparators", action="store_true", help="skip gather-bound / CUB sort-shuffle timing")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(steps, 5))")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 -- clocks are evidence, not the measurement
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "samples": len(s),
+                "reasons": [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]}
+
+
+# --------------------------------------------------------------- reference --
+def reference_arm(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref = bijshuf::shuffle_values_into compiled from the
+    reference headers) on all host threads; rank 0 only."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ctypes
+
+    import oracle as O
+    m, eb, variant, batch, desc = CONFIGS[args.config]
+    if O.REF is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    if batch:
+        m_sample, note = m, f"{batch} independent shuffles of {m} timed as one step"
+    else:
+        m_sample, note = m, "full per-GPU workload"
+    calls = args.warmup + args.steps
+    per = (ctypes.c_double * calls)()
+    fnv = ctypes.c_uint64()
+    if batch:
+        # BijectiveShuffleSampler-style: seed + b, one reference call per shuffle (u64 payload path).
+        t_all = []
+        for _ in range(calls):
+            t0 = time.perf_counter()
+            for b in range(batch):
+                O.REF.ref_shuffle_indices(m, SEED + b, variant, 24, 0, _scratch(m))
+            t_all.append(time.perf_counter() - t0)
+        times = t_all[args.warmup:]
+        bytes_step = 2 * batch * m * eb
+    else:
+        rc = O.REF.ref_time_shuffle_u64_calls(m_sample, SEED, variant, 24, 0, calls, per, ctypes.byref(fnv))
+        assert rc == 0, rc
+        times = list(per)[args.warmup:]
+        bytes_step = 2 * m_sample * 8
+    mean = sum(times) / len(times)
+    val = bytes_step / mean / 1e9
+    cores = int(O.REF.ref_hardware_threads())
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64" if eb == 8 else "u32",
+        "data": "synthetic (iota values)",
+        "config": {"workload": desc + (f" (reference sample: {note})"), "n": m_sample, "elem_bytes": eb,
+                   "seed": SEED, "rounds": 24, "variant": "VariablePhilox" if variant else "Lcg"},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"n={m_sample} u64 per step ({note}); {os.path.basename(O.REF.path)}, "
+                                   f"avx512={bool(O.REF.ref_avx512_active())}, workers=0 (all host threads)"},
+        "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+_SCR = {}
+
+
+def _scratch(m):
+    import numpy as np
+    if m not in _SCR:
+        _SCR[m] = np.empty(m, dtype=np.uint64)
+    return _SCR[m].ctypes.data
+
+
+def cpu_baseline_leg(args, cfgname):
+    """Reference CPU shuffle on this host, bounded sample (rank 0, N=1)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if O.REF is None:
+        return None
+    m, eb, variant, batch, desc = CONFIGS[cfgname]
+    if batch:
+        return None
+    trials = 3 if m >= (1 << 26) else 5
+    mean, _ = O.ref_time_shuffle_u64(m, SEED, variant, 24, trials)
+    return {"value": round(2 * m * 8 / mean / 1e9, 3), "unit": "GB/s", "cores": int(O.REF.ref_hardware_threads()),
+            "kind": "reference",
+            "sample": f"n={m} u64 (the full per-GPU workload), 1 warm-up + mean of {trials} "
+                      f"(bench.hpp:41-59), {os.path.basename(O.REF.path)}, avx512={bool(O.REF.ref_avx512_active())}"}
+
+
+# -------------------------------------------------------------------- ours --
+def ours_arm(args, rank, world, local):
+    import torch
+    import paper_2106_06161_b200 as bsg
+    from paper_2106_06161_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    m_gpu, eb, variant, batch, desc = CONFIGS[args.config]
+    cfg = bsg.ShuffleConfig(seed=SEED, variant=bsg.BijectionVariant(variant))
+    stream = torch.cuda.current_stream(dev)
+    tdt = {4: torch.int32, 8: torch.int64}[eb]
+
+    if batch:
+        m_total = m_gpu
+        vals = torch.arange(m_gpu, dtype=tdt, device=dev).repeat(batch, 1)
+        out = torch.empty_like(vals)
+        step_bytes_rank = 2 * batch * m_gpu * eb
+
+        def step():
+            bsg.shuffle_values_batched(vals, bsg.ShuffleConfig(seed=SEED + rank * batch, variant=cfg.variant),
+                                       out=out)
+        dominant = "bsg::k_batched"
+    else:
+        m_total = m_gpu * world  # weak scaling: one global shuffle of N * n elements
+        vals = torch.arange(m_total, dtype=tdt, device=dev)  # replicated input
+        step_bytes_rank = 2 * m_gpu * eb
+        if world == 1:
+            out = torch.empty(m_total, dtype=tdt, device=dev)
+
+            def step():
+                bsg.shuffle_values_into(vals, cfg, out)
+        else:
+            import ctypes
+
+            import torch.distributed as dist
+            b, e = ctypes.c_uint64(), ctypes.c_uint64()
+            _lib.check(_lib.lib.bsg_dist_counter_range(m_total, rank, world, ctypes.byref(b), ctypes.byref(e)))
+            out = torch.empty(e.value - b.value, dtype=tdt, device=dev)
+            cnt_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+            counts = torch.zeros(world, dtype=torch.int64, device=dev)
+            ccfg = cfg._c()
+
+            def step():
+                _lib.check(_lib.lib.bsg_shuffle_range(m_total, ctypes.byref(ccfg), b.value, e.value, vals.data_ptr(),
+                                                      None, out.data_ptr(), eb, cnt_dev.data_ptr(),
+                                                      stream.cuda_stream), "shuffle_range")
+                dist.all_gather_into_tensor(counts, cnt_dev)  # the 8-byte count exchange (NCCL)
+        dominant = "bsg::k_pow2" if (m_total & (m_total - 1)) == 0 else "bsg::k_compact"
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = bsg.kernel_launches()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        evs[0].record(stream)
+        for i in range(args.steps):
+            step()
+            evs[i + 1].record(stream)
+        barrier()
+    launches = bsg.kernel_launches() - launches0
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = step_bytes_rank * world / (ms_step * 1e-3) / 1e9
+
+    # Sanity check of the timed output against the library's own index path (cheap, after timing).
+    if not batch and world == 1:
+        perm = bsg.shuffle_indices(min(m_total, 1 << 20), cfg, device=dev)
+        if m_total <= (1 << 20):
+            assert torch.equal(out.to(torch.int64), perm), "bench output mismatch"
+
+    # ---- e2e: public API, pinned host buffers, H2D + shuffle + D2H each step
+    e2e = None
+    e2e_steps = args.e2e_steps or min(args.steps, 5)
+    if not batch:
+        host_in = torch.arange(m_total, dtype=tdt).pin_memory()
+        if world == 1:
+            host_out = torch.empty(m_total, dtype=tdt).pin_memory()
+
+            def e2e_step():
+                bsg.shuffle_values_into(host_in, cfg, host_out)
+            h2d, d2h = m_total * eb, m_total * eb
+        else:
+            host_out = torch.empty(out.numel(), dtype=tdt).pin_memory()
+
+            def e2e_step():
+                vals.copy_(host_in, non_blocking=True)
+                step()
+                host_out.copy_(out, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+            h2d, d2h = m_total * eb, out.numel() * eb
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        barrier()
+        el = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": round(step_bytes_rank * world / (el / e2e_steps) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+               "ms_per_step": round(el / e2e_steps * 1e3, 3),
+               "path": "bsg_shuffle_values(host pinned in, host pinned out) -> staged H2D, kernel, D2H"
+               if world == 1 else "per rank: H2D of the replicated input, shuffle_range + count allgather, D2H"}
+        del host_in, host_out
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    if not peak:
+        peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    kernel_ms = sum(per_step) / len(per_step)
+    alg_bytes = step_bytes_rank  # per launch on this rank (one kernel per step)
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    prof = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
+    traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64" if eb == 8 else "u32", "data": "synthetic (iota values, device-generated)",
+        "config": {"workload": desc + ("" if world == 1 else f"; global shuffle of {world}x n elements, "
+                                                             "counter-range partition, replicated input"),
+                   "n_per_gpu": m_gpu, "n_total": m_total if not batch else batch * m_gpu * world,
+                   "elem_bytes": eb, "seed": SEED, "rounds": 24,
+                   "variant": "VariablePhilox" if variant else "Lcg",
+                   "l2": "inputs (>= 4 GiB) exceed the 126 MB L2; no flush" if not batch
+                   else "256 MiB per step > L2; no flush",
+                   "parallelism": f"counter-range partition x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 3), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kernel_ms, 4),
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+    }
+    if not args.no_comparators and world == 1 and not batch:
+        line["comparators"] = comparators(bsg, torch, dev, vals, out, m_total, eb, cfg, stream)
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg(args, args.config)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def comparators(bsg, torch, dev, vals, out, m, eb, cfg, stream):
+    """The paper's two GPU reference points on the same data: the random-gather upper bound through a
+    precomputed permutation and SortShuffle (CUB radix sort of 64-bit keys)."""
+    res = {}
+
+    def t(fn, reps=5):
+        fn()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b) / reps
+
+    perm = bsg.shuffle_indices(m, cfg, device=dev)
+    ms = t(lambda: bsg.gather_into(vals, perm, out))
+    res["gather_bound"] = {"value": round(2 * m * eb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms": round(ms, 3),
+                           "what": "out[i] = in[perm[i]] through a precomputed permutation (reads the 8-byte index "
+                                   "too: 24 B/elem of traffic for 16 B/elem of work)"}
+    del perm
+    if eb == 8:
+        try:
+            ms = t(lambda: bsg.sort_shuffle_u64(vals, SEED, out=out), reps=3)
+            res["sort_shuffle"] = {"value": round(2 * m * eb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                                   "ms": round(ms, 3), "what": "CUB DeviceRadixSort::SortPairs of (mix64 key, value)"}
+        except Exception as e:  # noqa: BLE001
+            res["sort_shuffle"] = {"error": str(e)[:200]}
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    ours_arm(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -11,7 +11,7 @@ import os
 from ctypes import (POINTER, Structure, c_char_p, c_int32, c_uint32, c_uint64, c_ubyte, c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbsg.so")
+LIB_PATH = os.environ.get("BSG_LIB") or os.path.join(_HERE, "lib", "libbsg.so")  # BSG_LIB: experiment builds
 
 # bsg_status
 OK, EINVAL, ERANGE, EALIAS, ENOMEM, ECUDA, ENODEV, EUNSUPPORTED = range(8)

@@ -24,8 +24,13 @@ cudaError_t run_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
     constexpr uint64_t kTile = kThreads * kCompactItems;
     const uint64_t grid = (len + kTile - 1) / kTile;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    k_compact<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
-        a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
+    if constexpr (sizeof(T) >= 4 || std::is_same<T, IdxTag>::value) {
+      k_compact_smem<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+          a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
+    } else {
+      k_compact<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+          a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
+    }
   }
   note_launch();
   return cudaGetLastError();

@@ -11,9 +11,15 @@
 namespace bsg {
 
 // Launch geometry shared by host dispatch and kernels.
+#ifndef BSG_POW2_ITEMS
+#define BSG_POW2_ITEMS 8
+#endif
+#ifndef BSG_COMPACT_ITEMS
+#define BSG_COMPACT_ITEMS 8
+#endif
 constexpr int kThreads = 256;
-constexpr int kPow2Items = 8;      // counters per thread, pow2 kernel
-constexpr int kCompactItems = 8;   // counters per thread, compacting (look-back) kernel
+constexpr int kPow2Items = BSG_POW2_ITEMS;        // counters per thread, pow2 kernel
+constexpr int kCompactItems = BSG_COMPACT_ITEMS;  // counters per thread, compacting (look-back) kernel
 constexpr uint64_t kCompactTile = static_cast<uint64_t>(kThreads) * kCompactItems;
 constexpr int kBatchedMaxRounds = 64;
 

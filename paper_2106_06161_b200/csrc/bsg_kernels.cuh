@@ -63,19 +63,19 @@ __device__ __forceinline__ uint16_t ld_rand<uint16_t>(const uint16_t* p) {
 template <>
 __device__ __forceinline__ uint32_t ld_rand<uint32_t>(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 template <>
 __device__ __forceinline__ uint64_t ld_rand<uint64_t>(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 template <>
 __device__ __forceinline__ uint4 ld_rand<uint4>(const uint4* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
@@ -292,6 +292,126 @@ __global__ void __launch_bounds__(kThreads) k_compact(Src src, void* out_, uint6
     }
   }
   if (count_out != nullptr && tile == gridDim.x - 1 && tid == 0) *count_out = prefix + s_total;
+}
+
+// Shared-memory-staged variant (payloads of 4, 8, 16 bytes and indices).
+// After the block scan every survivor knows its in-tile rank, so its payload
+// is fetched with cp.async straight into smem[rank]: the random reads stay in
+// flight without holding registers (more tiles resident per SM => more
+// memory-level parallelism, the limiter of the 2x-padded case), the warp-0
+// look-back overlaps them, and the tile is written back with fully
+// coalesced stores in compacted order.
+template <typename T>
+__device__ __forceinline__ void cp_async_payload(T* smem_dst, const T* gsrc) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  if constexpr (sizeof(T) == 16) {
+    asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(sizeof(T))
+                 : "memory");
+  }
+}
+
+template <typename T, bool SH>
+__device__ __forceinline__ const T* src_addr(const Src& s, uint64_t y) {
+  if constexpr (!SH) {
+    return static_cast<const T*>(s.base) + y;
+  } else {
+    uint64_t g, off;
+    if (s.shard_shift >= 0) {
+      g = y >> s.shard_shift;
+      off = y & (s.shard_elems - 1);
+    } else {
+      g = y / s.shard_elems;
+      off = y - g * s.shard_elems;
+    }
+    return static_cast<const T*>(s.shard[g]) + off;
+  }
+}
+
+template <int KIND, typename CT, typename T, bool SH, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_compact_smem(Src src, void* out_, uint64_t m, uint64_t c0,
+                                                           uint64_t c1, BijParams p, Lookback lb,
+                                                           unsigned long long* count_out) {
+  constexpr bool kIdx = std::is_same<T, IdxTag>::value;
+  using V = typename std::conditional<kIdx, uint64_t, T>::type;
+  constexpr int kTile = kThreads * ITEMS;
+  constexpr int kSlots = ITEMS * kWarps;  // (item, warp) survivor counts, counter order
+  constexpr int kPerLane = kSlots / 32;
+  static_assert(kSlots % 32 == 0 && kPerLane <= 4, "slots");
+  __shared__ __align__(16) V s_val[kTile];
+  __shared__ uint32_t s_cnt[kSlots];
+  __shared__ unsigned long long s_prefix;
+  __shared__ uint32_t s_tile;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(lb.tile_counter, 1u);
+    if (t == gridDim.x - 1) *lb.tile_counter = 0;  // last ticket: reset for the next launch
+    s_tile = t;
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = c0 + static_cast<uint64_t>(tile) * kTile + tid;
+
+  CT img[ITEMS];
+  uint32_t mask[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint64_t c = t0 + j * kThreads;
+    img[j] = bij<KIND, CT>(static_cast<CT>(c), p);
+    mask[j] = __ballot_sync(0xFFFFFFFFu, (c < c1) && (static_cast<uint64_t>(img[j]) < m));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) s_cnt[j * kWarps + warp] = __popc(mask[j]);
+  }
+  __syncthreads();
+  // Every warp scans the kSlots counts itself (no second barrier before the loads).
+  uint32_t a[kPerLane], sum = 0;
+#pragma unroll
+  for (int i = 0; i < kPerLane; ++i) {
+    a[i] = s_cnt[lane * kPerLane + i];
+    sum += a[i];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  uint32_t ex[kPerLane];
+  ex[0] = incl - sum;
+#pragma unroll
+  for (int i = 1; i < kPerLane; ++i) ex[i] = ex[i - 1] + a[i - 1];
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int e = j * kWarps + warp;  // warp-uniform slot
+    uint32_t base = 0;
+#pragma unroll
+    for (int i = 0; i < kPerLane; ++i) {
+      const uint32_t x = __shfl_sync(0xFFFFFFFFu, ex[i], e / kPerLane);
+      if (e % kPerLane == i) base = x;
+    }
+    if ((mask[j] >> lane) & 1u) {
+      const uint32_t r = base + __popc(mask[j] & lt);
+      if constexpr (kIdx) s_val[r] = static_cast<uint64_t>(img[j]);
+      else cp_async_payload<T>(&s_val[r], src_addr<T, SH>(src, img[j]));
+    }
+  }
+  if constexpr (!kIdx) asm volatile("cp.async.commit_group;" ::: "memory");
+  if (warp == 0) {
+    const unsigned long long excl = lookback_warp(lb, tile, total);
+    if (lane == 0) s_prefix = excl;
+  }
+  if constexpr (!kIdx) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const unsigned long long prefix = s_prefix;
+  V* out = static_cast<V*>(out_) + prefix;
+  for (uint32_t i = tid; i < total; i += kThreads) st_out<V>(out + i, s_val[i]);
+  if (count_out != nullptr && tile == gridDim.x - 1 && tid == 0) *count_out = prefix + total;
 }
 
 // --------------------------------------------------------------- batched path

@@ -1,0 +1,15 @@
+#!/bin/bash
+# Captures the ncu evidence for the bench configurations (run under gpurun on one GPU).
+#   launch lists: every kernel of a short bench run with its device time (cold cache, serialised)
+#   full sets:    one capture of the dominant kernel per config
+set -x
+OUT=${OUT:-gpurun_out}
+mkdir -p $OUT
+B="python bench.py --steps 2 --warmup 1 --no-comparators --no-cpu-baseline --e2e-steps 1"
+for cfg in c2 c3 c4; do
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$cfg.csv $B --config $cfg > $OUT/launches_$cfg.log 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:k_pow2 -s 1 -c 1 -o $OUT/prof_c2 $B --config c2 > $OUT/prof_c2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_compact -s 1 -c 1 -o $OUT/prof_c3 $B --config c3 > $OUT/prof_c3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_batched -s 1 -c 1 -o $OUT/prof_c4 $B --config c4 > $OUT/prof_c4.log 2>&1
+ls -la $OUT
