@@ -144,6 +144,21 @@ bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_
 bsg_status bsg_ipc_open(const unsigned char handle[BSG_IPC_HANDLE_BYTES], void** dev_ptr_out);
 bsg_status bsg_ipc_close(void* dev_ptr);
 
+/* ------------------------------------------------- host-buffer pipeline --- */
+/* Streaming form of bsg_shuffle_values for HOST buffers: each submitted
+ * shuffle is H2D-copied, shuffled and D2H-copied on three internal streams
+ * with `depth` device staging slots, so the H2D of shuffle i+1 overlaps the
+ * D2H of shuffle i (PCIe is full duplex).  Host buffers should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous, and
+ * must stay untouched until bsg_pipeline_wait(ticket) returns.  Results are
+ * identical to bsg_shuffle_values. */
+typedef struct bsg_pipeline bsg_pipeline;
+bsg_status bsg_pipeline_create(uint64_t max_m, uint32_t elem_bytes, int32_t depth, bsg_pipeline** out);
+bsg_status bsg_pipeline_submit(bsg_pipeline* p, const void* host_in, void* host_out, uint64_t m,
+                               const bsg_config* cfg, uint64_t* ticket);
+bsg_status bsg_pipeline_wait(bsg_pipeline* p, uint64_t ticket);
+bsg_status bsg_pipeline_destroy(bsg_pipeline* p);
+
 /* ------------------------------------------------------------ baselines --- */
 /* The paper's SortShuffle (bench.hpp:109-156): random 64-bit
  * keys mix64(mix64(seed) + i*gamma) and a CUB radix sort of (key, value). */

@@ -42,7 +42,7 @@ __all__ = [
     "shuffle_values", "shuffle_values_into", "shuffle_values_batched", "gather", "gather_into",
     "compact_permutation", "mix64", "derive_round_keys", "LcgParams", "make_lcg", "lcg_apply",
     "VariablePhiloxParams", "make_philox", "philox_apply", "philox_invert", "bijection_apply", "sort_shuffle_u64",
-    "kernel_launches", "BsgError", "CudaError", "InvalidArgument", "OutOfRange", "Permutation",
+    "kernel_launches", "Pipeline", "BsgError", "CudaError", "InvalidArgument", "OutOfRange", "Permutation",
 ]
 
 Permutation = np.ndarray  # permutation.hpp:15 -- one-line notation, entry k = source index of slot k
@@ -320,6 +320,52 @@ def sort_shuffle_u64(values: Any, seed: int, out: Any = None):
         check(lib.bsg_sort_shuffle_u64(vb.ptr, ob.ptr, vb.nelem, seed & 0xFFFFFFFFFFFFFFFF, vb.stream()),
               "sort_shuffle")
     return out
+
+
+class Pipeline:
+    """Streaming shuffles of HOST buffers (bsg_pipeline_*): H2D of shuffle i+1 overlaps the D2H of shuffle i.
+
+    Host arrays should be pinned (torch `pin_memory()`); keep them alive and untouched until `wait(ticket)`.
+    """
+
+    def __init__(self, max_m: int, elem_bytes: int, depth: int = 2):
+        self._h = ctypes.c_void_p()
+        self._keep = {}
+        check(lib.bsg_pipeline_create(max_m, elem_bytes, depth, ctypes.byref(self._h)), "pipeline_create")
+        self.elem_bytes = elem_bytes
+
+    def submit(self, values: Any, out: Any, cfg: Optional[ShuffleConfig] = None) -> int:
+        cfg = cfg or ShuffleConfig()
+        vb, ob = _Buf(values), _Buf(out)
+        if vb.itemsize * vb.nelem != self.elem_bytes * vb.nelem or ob.nelem * ob.itemsize < vb.nelem * vb.itemsize:
+            raise InvalidArgument("pipeline: element size / output size mismatch")
+        t = ctypes.c_uint64()
+        check(lib.bsg_pipeline_submit(self._h, vb.ptr, ob.ptr, vb.nelem, ctypes.byref(cfg._c()), ctypes.byref(t)),
+              "pipeline_submit")
+        self._keep[t.value] = (values, out)
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        check(lib.bsg_pipeline_wait(self._h, ticket), "pipeline_wait")
+        self._keep.pop(ticket, None)
+
+    def close(self) -> None:
+        if self._h:
+            check(lib.bsg_pipeline_destroy(self._h), "pipeline_destroy")
+            self._h = ctypes.c_void_p()
+            self._keep.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def kernel_launches() -> int:

@@ -647,6 +647,108 @@ bsg_status bsg_sort_shuffle_u64(const uint64_t* in, uint64_t* out, uint64_t n, u
   });
 }
 
+}  // extern "C"
+
+struct bsg_pipeline {
+  struct Slot {
+    DevBuf din, dout;
+    cudaEvent_t h2d_done = nullptr, kernel_done = nullptr, d2h_done = nullptr;
+    uint64_t ticket = ~0ULL;
+  };
+  int device = 0;
+  uint64_t max_m = 0;
+  uint32_t eb = 0;
+  std::vector<Slot> slots;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  uint64_t next = 0;
+};
+
+extern "C" {
+
+bsg_status bsg_pipeline_create(uint64_t max_m, uint32_t elem_bytes, int32_t depth, bsg_pipeline** out) {
+  if (!out || elem_bytes == 0 || depth < 1 || depth > 8) return fail(BSG_EINVAL, "pipeline: bad arguments");
+  DeviceCtx* c = nullptr;
+  BSG_TRY(current_ctx(&c));
+  auto p = std::make_unique<bsg_pipeline>();
+  p->device = c->device;
+  p->max_m = max_m;
+  p->eb = elem_bytes;
+  p->slots.resize(static_cast<size_t>(depth));
+  const size_t bytes = std::max<uint64_t>(max_m, 1) * elem_bytes;
+  for (auto& s : p->slots) {
+    BSG_CUDA(s.din.ensure(bytes));
+    BSG_CUDA(s.dout.ensure(bytes));
+    BSG_CUDA(cudaEventCreateWithFlags(&s.h2d_done, cudaEventDisableTiming));
+    BSG_CUDA(cudaEventCreateWithFlags(&s.kernel_done, cudaEventDisableTiming));
+    BSG_CUDA(cudaEventCreateWithFlags(&s.d2h_done, cudaEventDisableTiming));
+  }
+  BSG_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+  BSG_CUDA(cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking));
+  BSG_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+  *out = p.release();
+  return BSG_OK;
+}
+
+bsg_status bsg_pipeline_submit(bsg_pipeline* p, const void* host_in, void* host_out, uint64_t m,
+                               const bsg_config* cfg_in, uint64_t* ticket) {
+  if (!p) return fail(BSG_EINVAL, "pipeline: null handle");
+  if (m > p->max_m) return fail(BSG_EINVAL, "pipeline: m exceeds the capacity given at creation");
+  if (host_in != nullptr && host_in == host_out) return fail(BSG_EALIAS, "shuffle_values_into: out aliases input");
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  const uint64_t t = p->next++;
+  auto& s = p->slots[t % p->slots.size()];
+  const size_t bytes = m * static_cast<size_t>(p->eb);
+  if (ticket) *ticket = t;
+  s.ticket = t;
+  if (m == 0) return BSG_OK;
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    // H2D into the slot once the slot's previous shuffle has consumed its input.
+    BSG_CUDA(cudaStreamWaitEvent(p->s_h2d, s.kernel_done, 0));
+    BSG_CUDA(cudaMemcpyAsync(s.din.p, host_in, bytes, cudaMemcpyHostToDevice, p->s_h2d));
+    BSG_CUDA(cudaEventRecord(s.h2d_done, p->s_h2d));
+    // Shuffle once the input landed and the slot's previous output left.
+    BSG_CUDA(cudaStreamWaitEvent(p->s_comp, s.h2d_done, 0));
+    BSG_CUDA(cudaStreamWaitEvent(p->s_comp, s.d2h_done, 0));
+    BSG_TRY(shuffle_device(c, s.din.p, s.dout.p, m, p->eb, cfg, p->s_comp));
+    BSG_CUDA(cudaEventRecord(s.kernel_done, p->s_comp));
+    // D2H of the result.
+    BSG_CUDA(cudaStreamWaitEvent(p->s_d2h, s.kernel_done, 0));
+    BSG_CUDA(cudaMemcpyAsync(host_out, s.dout.p, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+    BSG_CUDA(cudaEventRecord(s.d2h_done, p->s_d2h));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_pipeline_wait(bsg_pipeline* p, uint64_t ticket) {
+  if (!p) return fail(BSG_EINVAL, "pipeline: null handle");
+  if (ticket >= p->next) return fail(BSG_EINVAL, "pipeline: unknown ticket");
+  if (p->next - ticket > p->slots.size()) {  // slot reused since: its latest D2H completes later
+    BSG_CUDA(cudaStreamSynchronize(p->s_d2h));
+    return BSG_OK;
+  }
+  BSG_CUDA(cudaEventSynchronize(p->slots[ticket % p->slots.size()].d2h_done));
+  return BSG_OK;
+}
+
+bsg_status bsg_pipeline_destroy(bsg_pipeline* p) {
+  if (!p) return BSG_OK;
+  cudaStreamSynchronize(p->s_h2d);
+  cudaStreamSynchronize(p->s_comp);
+  cudaStreamSynchronize(p->s_d2h);
+  for (auto& s : p->slots) {
+    s.din.release();
+    s.dout.release();
+    cudaEventDestroy(s.h2d_done);
+    cudaEventDestroy(s.kernel_done);
+    cudaEventDestroy(s.d2h_done);
+  }
+  cudaStreamDestroy(p->s_h2d);
+  cudaStreamDestroy(p->s_comp);
+  cudaStreamDestroy(p->s_d2h);
+  delete p;
+  return BSG_OK;
+}
+
 const char* bsg_status_string(bsg_status s) {
   switch (s) {
     case BSG_OK: return "ok";

@@ -1,0 +1,148 @@
+"""Multi-GPU bijective shuffle: one process per GPU, torch.distributed for the
+plumbing (NCCL on GPUs; gloo works for the host logic).
+
+The scheme of the north star:
+  1. the padded counter domain [0, 2^bits) is split into `world` contiguous
+     ranges (bsg_dist_counter_range);
+  2. each rank runs the fused kernel on its range (bsg_shuffle_range): the
+     survivors of a range are a contiguous run of the global output, written
+     to the rank's local buffer in counter order;
+  3. ranks all-gather their survivor counts (one u64 per rank -- an 8-element
+     NCCL all-gather) and take the exclusive prefix as their global offset;
+  4. optionally `rebalance` moves the pieces into equal contiguous output
+     shards with one all-to-all of contiguous runs (only boundary slack moves).
+Payload reads go to the local replica, or to peer HBM over NVLink through
+CUDA-IPC-mapped shard pointers when the input is sharded (`ipc_shards`).
+The output is bit-identical to the single-GPU shuffle of all m elements.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Callable, List, Optional, Sequence, Tuple
+
+from . import ShuffleConfig, _lib
+from ._lib import check, lib
+
+
+def counter_range(m: int, rank: int, world: int) -> Tuple[int, int]:
+    """Counter range [begin, end) of the padded domain owned by `rank`."""
+    b, e = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.bsg_dist_counter_range(m, rank, world, ctypes.byref(b), ctypes.byref(e)), "dist_counter_range")
+    return b.value, e.value
+
+
+def offsets_from_counts(counts: Sequence[int], rank: int) -> int:
+    """Exclusive prefix of the gathered survivor counts: this rank's first global output position."""
+    return int(sum(int(c) for c in counts[:rank]))
+
+
+def equal_shards(m: int, world: int) -> List[Tuple[int, int]]:
+    """Target layout for `rebalance`: contiguous, near-equal output shards."""
+    base, rem = divmod(m, world)
+    out, start = [], 0
+    for r in range(world):
+        n = base + (1 if r < rem else 0)
+        out.append((start, start + n))
+        start += n
+    return out
+
+
+def transfer_plan(counts: Sequence[int], m: int, world: int) -> List[List[int]]:
+    """send[src][dst] = elements rank src sends to rank dst so that piece
+    [off_src, off_src + count_src) lands in the equal shards."""
+    shards = equal_shards(m, world)
+    plan = [[0] * world for _ in range(world)]
+    off = 0
+    for src, c in enumerate(counts):
+        lo, hi = off, off + int(c)
+        for dst, (a, b) in enumerate(shards):
+            ov = min(hi, b) - max(lo, a)
+            if ov > 0:
+                plan[src][dst] = ov
+        off = hi
+    return plan
+
+
+def _gpu_range(m: int, cfg: ShuffleConfig, begin: int, end: int, values, out, shards=None) -> int:
+    """Fused kernel on one counter range; returns the survivor count (device path, current stream)."""
+    import torch
+    count = ctypes.c_uint64()
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    elem = out.element_size()
+    check(lib.bsg_shuffle_range(m, ctypes.byref(cfg._c()), begin, end,
+                                values.data_ptr() if values is not None else None,
+                                ctypes.byref(shards) if shards is not None else None, out.data_ptr(), elem,
+                                ctypes.addressof(count), stream), "shuffle_range")
+    return count.value
+
+
+def shuffle_values(values, m: int, cfg: Optional[ShuffleConfig] = None, group=None, out=None, shards=None,
+                   range_fn: Optional[Callable] = None):
+    """Distributed shuffle of m elements.
+
+    values: the full input replicated on this rank (or None with `shards` from `ipc_shards`).
+    Returns (piece, global_offset, counts): piece[:counts[rank]] are global output positions
+    [global_offset, global_offset + counts[rank]).
+    `range_fn(m, cfg, begin, end, values, out) -> count` replaces the GPU kernel (tests inject the oracle).
+    """
+    import torch
+    import torch.distributed as dist
+    cfg = cfg or ShuffleConfig()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if m <= 2:
+        raise _lib.InvalidArgument("distributed shuffle needs m >= 3")
+    begin, end = counter_range(m, rank, world)
+    if out is None:
+        like = values if values is not None else None
+        dtype = like.dtype if like is not None else torch.int64
+        device = like.device if like is not None else torch.device("cuda", torch.cuda.current_device())
+        out = torch.empty(end - begin, dtype=dtype, device=device)
+    fn = range_fn or (lambda *a: _gpu_range(*a, shards=shards))
+    cnt = fn(m, cfg, begin, end, values, out)
+    dev = out.device
+    mine = torch.tensor([cnt], dtype=torch.int64, device=dev)
+    allc = torch.zeros(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allc, mine, group=group)  # the 8-byte-per-rank count exchange
+    counts = [int(x) for x in allc.tolist()]
+    if sum(counts) != m:
+        raise _lib.CudaError(f"survivor counts {counts} do not sum to m={m}")
+    return out, offsets_from_counts(counts, rank), counts
+
+
+def rebalance(piece, counts: Sequence[int], m: int, group=None):
+    """Move the per-rank pieces into equal contiguous output shards (one all-to-all of contiguous runs)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    plan = transfer_plan(counts, m, world)
+    send = plan[rank]
+    recv = [plan[src][rank] for src in range(world)]
+    out = torch.empty(sum(recv), dtype=piece.dtype, device=piece.device)
+    dist.all_to_all_single(out, piece[:counts[rank]].contiguous(), output_split_sizes=recv,
+                           input_split_sizes=send, group=group)
+    return out
+
+
+def ipc_shards(local_shard, group=None) -> "_lib.bsg_shards":
+    """Exchange CUDA IPC handles of each rank's equally sized input shard and map every peer's shard
+    (NVLink peer reads).  Returns the bsg_shards table for `shuffle_values(..., shards=...)`."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    h = (ctypes.c_ubyte * 64)()
+    check(lib.bsg_ipc_export(local_shard.data_ptr(), h), "ipc_export")
+    handles = [None] * world
+    dist.all_gather_object(handles, (bytes(h), local_shard.numel()), group=group)
+    tab = _lib.bsg_shards()
+    sizes = {n for _, n in handles}
+    if len(sizes) != 1:
+        raise _lib.InvalidArgument("input shards must be equally sized")
+    for g, (hb, _) in enumerate(handles):
+        if g == rank:
+            tab.ptrs[g] = local_shard.data_ptr()
+            continue
+        p = ctypes.c_void_p()
+        check(lib.bsg_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(hb), ctypes.byref(p)), "ipc_open")
+        tab.ptrs[g] = p.value
+    tab.count = world
+    tab.shard_elems = sizes.pop()
+    return tab

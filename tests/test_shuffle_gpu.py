@@ -375,3 +375,18 @@ def test_kernel_launch_counter_moves(bsg, cuda):
     bsg.shuffle_indices(1 << 20, cfg_of(bsg), device="cuda")
     cuda.cuda.synchronize()
     assert bsg.kernel_launches() > before
+
+
+def test_pipeline_streams_match_oracle(bsg, cuda):
+    m = (1 << 20) + 3
+    pairs = [(cuda.arange(m, dtype=cuda.int64).pin_memory(), cuda.empty(m, dtype=cuda.int64).pin_memory())
+             for _ in range(3)]
+    with bsg.Pipeline(m, 8, depth=2) as pipe:
+        tickets = [pipe.submit(pairs[i][0], pairs[i][1], cfg_of(bsg, seed=40 + i)) for i in range(3)]
+        for t in tickets:
+            pipe.wait(t)
+    for i in range(3):
+        assert np.array_equal(pairs[i][1].numpy().view(np.uint64), O.shuffle_indices(m, 40 + i)), i
+    with pytest.raises(bsg.InvalidArgument):
+        with bsg.Pipeline(16, 8) as pipe:
+            pipe.submit(pairs[0][0], pairs[0][1])  # m exceeds capacity
