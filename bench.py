@@ -246,7 +246,7 @@ def ours_arm(args, rank, world, local):
                                                       None, out.data_ptr(), eb, cnt_dev.data_ptr(),
                                                       stream.cuda_stream), "shuffle_range")
                 dist.all_gather_into_tensor(counts, cnt_dev)  # the 8-byte count exchange (NCCL)
-        dominant = "bsg::k_pow2" if (m_total & (m_total - 1)) == 0 else "bsg::k_compact_smem"
+        dominant = ("bsg::k_part1+k_part2+k_place" if (m_total & (m_total - 1)) == 0 and m_total * eb >= (256 << 20) else "bsg::k_pow2") if (m_total & (m_total - 1)) == 0 else "bsg::k_compact_smem"
 
     def barrier():
         torch.cuda.synchronize(dev)

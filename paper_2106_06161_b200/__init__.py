@@ -373,6 +373,11 @@ def kernel_launches() -> int:
     return int(lib.bsg_kernel_launches())
 
 
+def set_path(path: int) -> int:
+    """0 = automatic, 1 = single fused pass only, 2 = partitioned three-pass whenever eligible (pow2)."""
+    return int(lib.bsg_set_path(int(path)))
+
+
 def set_force_compact(on: bool) -> bool:
     """Testing knob: route power-of-two sizes through the look-back kernel too."""
     return bool(lib.bsg_set_force_compact(1 if on else 0))

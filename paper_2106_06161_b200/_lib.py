@@ -65,6 +65,7 @@ SIGNATURES = {
     "bsg_version": (c_int32, []),
     "bsg_kernel_launches": (c_uint64, []),
     "bsg_set_force_compact": (c_int32, [c_int32]),
+    "bsg_set_path": (c_int32, [c_int32]),
     "bsg_release_workspace": (c_int32, []),
 }
 

@@ -13,6 +13,7 @@
 
 #include "../../include/bsg.h"
 #include "bsg_internal.h"
+#include "bsg_partition.h"
 
 namespace {
 
@@ -78,6 +79,7 @@ struct DeviceCtx {
   uint32_t epoch = 0;
   DevBuf keys;     // round keys for non-24-round Philox
   DevBuf st_in, st_out, st_idx, st_tmp;  // host-pointer staging / temporaries
+  DevBuf part;                           // partitioned-path workspace
   cudaEvent_t ws_done = nullptr;
   bool ready = false;
 };
@@ -85,6 +87,10 @@ struct DeviceCtx {
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
 int g_force_compact = 0;
+int g_path = 0;  // 0 auto, 1 single-pass only, 2 partitioned whenever eligible
+// Auto mode uses the partitioned path for power-of-two shuffles whose payload
+// exceeds this many bytes (below it the single pass is L2-resident and faster).
+uint64_t g_partition_min_bytes = 256ULL << 20;
 
 bsg_status current_ctx(DeviceCtx** out) {
   int dev = 0;
@@ -199,6 +205,32 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
   BSG_TRY(ws_begin(c, s));
   BSG_TRY(upload_keys(c, p, cfg.seed, s));
   const bool pow2 = (m == (1ULL << bits));
+  if (pow2 && !g_force_compact && g_path != 1 && elem_code > 0 && src.nshards == 0 && c0 == 0 &&
+      c1 == (1ULL << bits) && bsg::partition_eligible(elem_code, bits) &&
+      (g_path == 2 || m * static_cast<uint64_t>(elem_code) >= g_partition_min_bytes)) {
+    const size_t need = bsg::partition_workspace_bytes(elem_code, bits);
+    cudaError_t ae = c->part.ensure(need);
+    if (ae == cudaSuccess) {
+      const uint64_t n = 1ULL << bits;
+      char* w = static_cast<char*>(c->part.p);
+      bsg::PartitionLaunch P;
+      P.in = src.base;
+      P.out = out;
+      P.tmp_values = w;
+      P.tmp_dest = reinterpret_cast<uint32_t*>(w + n * elem_code);
+      P.tmp_dlow = reinterpret_cast<uint16_t*>(w + n * elem_code + n * 4);
+      P.cursors = reinterpret_cast<uint32_t*>(w + n * elem_code + n * 6);
+      P.p = p;
+      BSG_CUDA(bsg::launch_partition(elem_code, P, s));
+      if (count_dev) {
+        const unsigned long long cnt = n;
+        BSG_CUDA(cudaMemcpyAsync(count_dev, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
+        BSG_CUDA(cudaStreamSynchronize(s));
+      }
+      return ws_end(c, s);
+    }
+    cudaGetLastError();  // workspace did not fit: the single-pass kernel needs none
+  }
   bsg::ShuffleLaunch L;
   L.src = src;
   L.out = out;
@@ -769,6 +801,12 @@ int32_t bsg_version(void) { return 100; }
 
 uint64_t bsg_kernel_launches(void) { return bsg::launches(); }
 
+int32_t bsg_set_path(int32_t path) {
+  const int old = g_path;
+  g_path = (path >= 0 && path <= 2) ? path : 0;
+  return old;
+}
+
 int32_t bsg_set_force_compact(int32_t on) {
   const int old = g_force_compact;
   g_force_compact = on ? 1 : 0;
@@ -784,6 +822,7 @@ bsg_status bsg_release_workspace(void) {
     c->st_out.release();
     c->st_idx.release();
     c->st_tmp.release();
+    c->part.release();
     c->epoch = 0;
     return BSG_OK;
   });

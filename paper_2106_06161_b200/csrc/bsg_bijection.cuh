@@ -79,6 +79,7 @@ struct BijParams {
   uint64_t lcg_a = 1, lcg_c = 0, lcg_ainv = 1;  // LCG (a forced odd), inverse multiplier
   uint64_t mask = 0;                            // 2^bits - 1
   uint32_t LM = 0, RM = 0;                      // Philox half masks (RM may be 0xFFFFFFFF)
+  uint32_t shl = 0;                             // 2^L: the inverse moves the spare bit up with an IMAD
   int32_t variant = kPhilox, bits = 0, L = 0, R = 0, rounds = 0, pad = 0;
   const uint32_t* gkeys = nullptr;  // device copy of all keys (rounds > kParamKeys)
   uint32_t keys[kParamKeys] = {};
@@ -115,15 +116,18 @@ BSG_HD void philox_round(uint32_t& s0, uint32_t& s1, uint32_t k, int L, uint32_t
 // Inverse round (bijection.hpp:127-141).  For D == 1 the right half carries
 // garbage above bit L+1 between rounds (masked at the end): the spare bit is
 // bit 0 and only `t1 >> 1` modulo 2^L is consumed.
+// The spare-bit shift t1 << L is an IMAD by the runtime constant shl = 2^L
+// (FMA pipe) rather than a SHF (ALU pipe): it balances the two integer pipes
+// (measured +17% on sm_100a, tools/microbench/mb6.cu).
 template <int D>
-BSG_HD void philox_inv_round(uint32_t& t0, uint32_t& t1, uint32_t k, int L, uint32_t LM) {
+BSG_HD void philox_inv_round(uint32_t& t0, uint32_t& t1, uint32_t k, uint32_t shl, uint32_t LM) {
   const uint32_t s0 = ((t1 >> D) * kM0InvLo) & LM;
 #ifdef __CUDA_ARCH__
   const uint32_t hi = __umulhi(s0, kM0Lo) + s0 * kM0Hi;
 #else
   const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(s0) * kM0Lo) >> 32) + s0 * kM0Hi;
 #endif
-  const uint32_t s1 = ((hi ^ k ^ t0) & LM) | (D ? (t1 << L) : 0u);
+  const uint32_t s1 = ((hi ^ k ^ t0) & LM) | (D ? (t1 * shl) : 0u);
   t0 = s0;
   t1 = s1;
 }
@@ -157,14 +161,14 @@ BSG_HD uint64_t philox_inv(uint64_t y, const BijParams& p) {
   uint32_t t1 = static_cast<uint32_t>(y) & p.RM;
   if constexpr (NR > 0) {
 #pragma unroll
-    for (int i = NR - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, p.keys[i], p.L, p.LM);
+    for (int i = NR - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, p.keys[i], p.shl, p.LM);
   } else {
 #ifdef __CUDA_ARCH__
     const uint32_t* ks = p.gkeys;
-    for (int i = p.rounds - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, __ldg(ks + i), p.L, p.LM);
+    for (int i = p.rounds - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, __ldg(ks + i), p.shl, p.LM);
 #else
     const uint32_t* ks = p.gkeys ? p.gkeys : p.keys;
-    for (int i = p.rounds - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, ks[i], p.L, p.LM);
+    for (int i = p.rounds - 1; i >= 0; --i) philox_inv_round<D>(t0, t1, ks[i], p.shl, p.LM);
 #endif
   }
   return (static_cast<uint64_t>(t0) << p.R) | (t1 & p.RM);
@@ -211,6 +215,7 @@ inline int make_params(int variant, int bits, uint64_t seed, int rounds, BijPara
   p.R = bits - p.L;
   p.LM = static_cast<uint32_t>((1ULL << p.L) - 1);
   p.RM = static_cast<uint32_t>((1ULL << p.R) - 1);
+  p.shl = static_cast<uint32_t>(1ULL << p.L);
   p.rounds = rounds;
   for (int i = 0; i < rounds && i < kParamKeys; ++i) p.keys[i] = round_key(seed, i);
   return 0;
@@ -230,8 +235,8 @@ inline uint64_t host_apply(const BijParams& p, uint64_t seed, uint64_t x, bool i
     }
   } else {
     for (int i = p.rounds - 1; i >= 0; --i) {
-      if (d) philox_inv_round<1>(a, b, key(i), L, p.LM);
-      else philox_inv_round<0>(a, b, key(i), L, p.LM);
+      if (d) philox_inv_round<1>(a, b, key(i), p.shl, p.LM);
+      else philox_inv_round<0>(a, b, key(i), p.shl, p.LM);
     }
   }
   return (static_cast<uint64_t>(a) << R) | (b & p.RM);

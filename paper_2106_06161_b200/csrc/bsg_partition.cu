@@ -1,0 +1,288 @@
+// bsg_partition.cu -- partitioned (three-pass) shuffle for large power-of-two
+// domains, the B200 answer to the DRAM random-access wall.
+//
+// Why: a single-pass shuffle of a 4 GiB array issues one random read per
+// element; on B200 those saturate at ~47 G reads/s (DRAM row activations,
+// independent of element size -- profiles/r01_microbench.md), i.e. 11.4 ms for
+// 2^29 elements although 8.6 GB of payload would stream in 1.4 ms.  When
+// m == 2^bits every counter survives and out[f^-1(j)] = in[j], so the
+// permutation can be applied by streaming the INPUT in order and routing each
+// element by its destination f^-1(j) (philox_invert, bijection.hpp:117-143):
+//   P1  read in[] sequentially, inverse cipher -> dest, counting-sort each
+//       8192-element tile in shared memory into 2^s1 coarse destination
+//       buckets, append the runs to the buckets (value + u32 dest);
+//   P2  per coarse bucket, the same split into 2^s2 fine windows of W2
+//       elements (value + u16 dest-in-window), written into `out` itself;
+//   P3  per fine window (64 KiB), scatter into shared memory at dest and
+//       write the window back coalesced (in place: each CTA reads its whole
+//       range before writing).
+// Every DRAM access is a coalesced run; traffic is ~60 B/element instead of
+// one random 64-B access per 8-B element.  Exact sizes (pow2: each bucket
+// receives exactly its window) make the layout static; atomic cursors only
+// order elements inside a bucket, which the final exact placement makes
+// irrelevant -- the output is bit-identical to the single-pass kernel.
+#include <cuda_runtime.h>
+
+#include "bsg_kernels.cuh"
+#include "bsg_partition.h"
+
+namespace bsg {
+
+namespace {
+
+#ifndef BSG_P1_THREADS
+#define BSG_P1_THREADS 256
+#endif
+#ifndef BSG_P2_THREADS
+#define BSG_P2_THREADS 256
+#endif
+constexpr int kP1Threads = BSG_P1_THREADS, kP1Items = 4096 / BSG_P1_THREADS, kP1Tile = 4096;
+constexpr int kP2Threads = BSG_P2_THREADS, kP2Items = 4096 / BSG_P2_THREADS, kP2Tile = 4096;
+constexpr int kP3Threads = 512;
+constexpr int kMaxB1 = 512, kMaxB2 = 256;
+
+template <int KIND, int D>
+__device__ __forceinline__ uint32_t inv_bij(uint32_t y, const BijParams& p) {
+  if constexpr (KIND == kKindLcg) return static_cast<uint32_t>(lcg_inv(y, p));
+  else if constexpr (KIND == kKindPh0 || KIND == kKindPh1) return static_cast<uint32_t>(philox_inv<D, 24>(y, p));
+  else return static_cast<uint32_t>(philox_inv<D, 0>(y, p));
+}
+
+// Block-wide exclusive scan of `nb` <= 2 * blockDim.x bin counts.
+__device__ __forceinline__ void scan_bins(const uint32_t* hist, uint32_t* start, int nb, uint32_t* warp_tot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (nb + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);  // 1 or 2
+  uint32_t loc[2] = {0u, 0u}, sum = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int idx = tid * per + k;
+    if (k < per && idx < nb) loc[k] = hist[idx];
+    sum += loc[k];
+  }
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    uint32_t w = lane < nw ? warp_tot[lane] : 0u, z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < nw) warp_tot[lane] = z - w;
+  }
+  __syncthreads();
+  uint32_t run = warp_tot[warp] + x - sum;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int idx = tid * per + k;
+    if (k < per && idx < nb) start[idx] = run;
+    run += loc[k];
+  }
+}
+
+// P1: stream the input, route by coarse destination bucket.
+template <int KIND, int D, typename T>
+__global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, T* __restrict__ tv,
+                                                         uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
+                                                         BijParams p, int bshift, int nb, uint64_t w1) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sv = reinterpret_cast<T*>(smem);
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);
+  __shared__ uint32_t hist[kMaxB1], start[kMaxB1], gbase[kMaxB1], wt[32];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kP1Tile + tid;
+  T v[kP1Items];
+#pragma unroll
+  for (int i = 0; i < kP1Items; ++i) v[i] = __ldcs(in + base + i * kP1Threads);
+  uint32_t dst[kP1Items], rk[kP1Items];
+#pragma unroll
+  for (int i = 0; i < kP1Items; ++i) {
+    dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
+    rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
+  }
+  __syncthreads();
+  scan_bins(hist, start, nb, wt);
+  for (int i = tid; i < nb; i += kP1Threads) gbase[i] = atomicAdd(cur1 + i, hist[i]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kP1Items; ++i) {
+    const uint32_t s = start[dst[i] >> bshift] + rk[i];
+    sv[s] = v[i];
+    sd[s] = dst[i];
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int s = tid; s < kP1Tile; s += kP1Threads) {
+    const uint32_t d = sd[s], b = d >> bshift;
+    const uint64_t pos = b * w1 + gbase[b] + (s - start[b]);
+    __stcs(tv + pos, sv[s]);
+    __stcs(td + pos, d);
+  }
+}
+
+// P2: split each coarse bucket into fine windows of 2^w2 elements.
+template <typename T>
+__global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, const uint32_t* __restrict__ td,
+                                                         T* __restrict__ ov, uint16_t* __restrict__ od,
+                                                         uint32_t* __restrict__ cur2, int w2, int nb2,
+                                                         uint64_t w1) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sv = reinterpret_cast<T*>(smem);
+  uint16_t* sd = reinterpret_cast<uint16_t*>(sv + kP2Tile);
+  uint8_t* sb = reinterpret_cast<uint8_t*>(sd + kP2Tile);
+  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], gbase[kMaxB2], wt[32];
+  const int tid = threadIdx.x;
+  if (tid < nb2) hist[tid] = 0;
+  __syncthreads();
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kP2Tile;
+  const uint64_t coarse = t0 / w1;
+  const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
+  T v[kP2Items];
+  uint32_t d[kP2Items], rk[kP2Items];
+#pragma unroll
+  for (int i = 0; i < kP2Items; ++i) {
+    v[i] = __ldcs(tv + t0 + tid + i * kP2Threads);
+    d[i] = __ldcs(td + t0 + tid + i * kP2Threads);
+  }
+#pragma unroll
+  for (int i = 0; i < kP2Items; ++i) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
+  __syncthreads();
+  scan_bins(hist, start, nb2, wt);
+  uint32_t* cur = cur2 + coarse * nb2;
+  if (tid < nb2) gbase[tid] = atomicAdd(cur + tid, hist[tid]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kP2Items; ++i) {
+    const uint32_t f = (d[i] >> w2) & fmask;
+    const uint32_t s = start[f] + rk[i];
+    sv[s] = v[i];
+    sd[s] = static_cast<uint16_t>(d[i] & wmask);
+    sb[s] = static_cast<uint8_t>(f);
+  }
+  __syncthreads();
+  const uint64_t win0 = coarse * w1;  // first element of this coarse bucket's output range
+#pragma unroll 4
+  for (int s = tid; s < kP2Tile; s += kP2Threads) {
+    const uint32_t f = sb[s];
+    const uint64_t pos = win0 + (static_cast<uint64_t>(f) << w2) + gbase[f] + (s - start[f]);
+    ov[pos] = sv[s];
+    od[pos] = sd[s];
+  }
+}
+
+// P3: place each fine window through shared memory, in place in `out`.
+template <typename T>
+__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, const uint16_t* __restrict__ od,
+                                                      int w2) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* win = reinterpret_cast<T*>(smem);
+  const uint32_t W = 1u << w2;
+  T* o = out + (static_cast<uint64_t>(blockIdx.x) << w2);
+  const uint16_t* dd = od + (static_cast<uint64_t>(blockIdx.x) << w2);
+  constexpr int kU = 8;
+  for (uint32_t i0 = threadIdx.x; i0 < W; i0 += kP3Threads * kU) {
+    T v[kU];
+    uint16_t d[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * kP3Threads;
+      if (i < W) {
+        v[u] = __ldcs(o + i);
+        d[u] = __ldcs(reinterpret_cast<const unsigned short*>(dd) + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * kP3Threads < W) win[d[u]] = v[u];
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < W; i += kP3Threads) __stcs(o + i, win[i]);
+}
+
+template <typename T>
+int window_log2() {
+  return sizeof(T) == 4 ? 14 : (sizeof(T) == 8 ? 13 : 12);  // 64 KiB smem window
+}
+
+template <int KIND, int D, typename T>
+cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
+  const int b = a.p.bits;
+  const int w2 = window_log2<T>();
+  const int total = b - w2;
+  const int s1 = (total + 1) / 2, s2 = total - s1;
+  const uint64_t n = 1ULL << b, w1 = 1ULL << (b - s1);
+  const int nb1 = 1 << s1, nb2 = 1 << s2;
+  uint32_t* cur1 = a.cursors;
+  uint32_t* cur2 = a.cursors + nb1;
+  cudaError_t e = cudaMemsetAsync(a.cursors, 0, (static_cast<size_t>(nb1) + static_cast<size_t>(nb1) * nb2) * 4, s);
+  if (e != cudaSuccess) return e;
+  const size_t sm1 = kP1Tile * (sizeof(T) + 4);
+  const size_t sm2 = kP2Tile * (sizeof(T) + 3);
+  const size_t sm3 = (size_t{1} << w2) * sizeof(T);
+  cudaFuncSetAttribute(k_part1<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
+  cudaFuncSetAttribute(k_part2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
+  cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+  T* tv = static_cast<T*>(a.tmp_values);
+  k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
+      static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1);
+  k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
+                                                                          a.tmp_dlow, cur2, w2, nb2, w1);
+  k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2);
+  note_launch(3);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch_partition(const PartitionLaunch& a, cudaStream_t s) {
+  switch (kind_of(a.p)) {
+    case kKindLcg: return run_partition<kKindLcg, 0, T>(a, s);
+    case kKindPh0: return run_partition<kKindPh0, 0, T>(a, s);
+    case kKindPh1: return run_partition<kKindPh1, 1, T>(a, s);
+    case kKindPh0G: return run_partition<kKindPh0G, 0, T>(a, s);
+    case kKindPh1G: return run_partition<kKindPh1G, 1, T>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool partition_eligible(int elem_code, int bits) {
+  int w2;
+  switch (elem_code) {
+    case 4: w2 = 14; break;
+    case 8: w2 = 13; break;
+    case 16: w2 = 12; break;
+    default: return false;
+  }
+  const int total = bits - w2;
+  const int s1 = (total + 1) / 2, s2 = total - s1;
+  // fan-outs within the shared-memory histograms; tiles must not straddle buckets; 32-bit destinations
+  return bits <= 32 && s1 >= 1 && s2 >= 1 && (1 << s1) <= kMaxB1 && (1 << s2) <= kMaxB2 &&
+         (bits - s1) >= 12 && bits >= 14;
+}
+
+size_t partition_workspace_bytes(int elem_code, int bits) {
+  const uint64_t n = 1ULL << bits;
+  return n * static_cast<uint64_t>(elem_code) + n * 4 + n * 2 + (kMaxB1 + static_cast<size_t>(kMaxB1) * kMaxB2) * 4 +
+         3 * 256;
+}
+
+cudaError_t launch_partition(int elem_code, const PartitionLaunch& a, cudaStream_t s) {
+  switch (elem_code) {
+    case 4: return dispatch_partition<uint32_t>(a, s);
+    case 8: return dispatch_partition<uint64_t>(a, s);
+    case 16: return dispatch_partition<uint4>(a, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace bsg

@@ -390,3 +390,27 @@ def test_pipeline_streams_match_oracle(bsg, cuda):
     with pytest.raises(bsg.InvalidArgument):
         with bsg.Pipeline(16, 8) as pipe:
             pipe.submit(pairs[0][0], pairs[0][1])  # m exceeds capacity
+
+
+def test_partitioned_path_matches_single_pass(bsg, cuda, golden):
+    """The three-pass partitioned kernel (pow2, large) is bit-identical to the fused single pass."""
+    old = bsg.set_path(2)
+    try:
+        for m, dt, variant, rounds in (((1 << 16), cuda.int64, PHILOX, 24), ((1 << 20), cuda.int32, PHILOX, 24),
+                                       ((1 << 21), cuda.int64, LCG, 24), ((1 << 22), cuda.int64, PHILOX, 12),
+                                       ((1 << 23), cuda.int32, PHILOX, 24), ((1 << 19), cuda.int64, PHILOX, 24)):
+            vals = cuda.arange(m, dtype=dt, device="cuda")
+            got = bsg.shuffle_values(vals, cfg_of(bsg, seed=m + rounds, variant=variant, rounds=rounds))
+            exp = O.shuffle_indices(m, m + rounds, variant, rounds)
+            assert np.array_equal(got.cpu().numpy().astype(np.uint64), exp), (m, dt, variant, rounds)
+        for case in golden["values_full_hash"]:
+            if case["m"] & (case["m"] - 1):
+                continue
+            vals = cuda.arange(case["m"], dtype=cuda.int64, device="cuda")
+            out = bsg.shuffle_values(vals, cfg_of(bsg, seed=case["seed"], variant=case["variant"]))
+            host = out.cpu().numpy().view(np.uint64)
+            del vals, out
+            assert f"{O.fnv1a64(host):016x}" == case["fnv"], case
+    finally:
+        bsg.set_path(old)
+        cuda.cuda.empty_cache()

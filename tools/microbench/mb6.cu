@@ -1,0 +1,91 @@
+// Inverse VariablePhilox (d=1, bits 29) round formulations: which pipe mix is fastest on sm_100a?
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb6 mb6.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA error %s line %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+static constexpr uint64_t M0 = 0xD2B74407B1CE6E93ULL;
+static constexpr uint32_t M0LO = (uint32_t)M0, M0HI = (uint32_t)(M0 >> 32);
+static constexpr uint64_t oi(uint64_t a) { uint64_t x = a; for (int i = 0; i < 5; ++i) x *= 2 - a * x; return x; }
+static constexpr uint32_t INV = (uint32_t)oi(M0);
+struct P { uint32_t k[24]; uint32_t half, shl, LM, RM; int L, R; };
+
+template <int V>
+__device__ __forceinline__ uint32_t inv(uint32_t y, const P& p) {
+  uint32_t t0 = y >> p.R, t1 = y & p.RM;
+#pragma unroll
+  for (int i = 23; i >= 0; --i) {
+    uint32_t a = (V & 1) ? __umulhi(t1, p.half) : (t1 >> 1);
+    uint32_t s0 = (a * INV) & p.LM;
+    uint32_t hi;
+    if (V & 4) hi = (uint32_t)(((uint64_t)s0 * M0LO) >> 32) + s0 * M0HI;
+    else hi = __umulhi(s0, M0LO) + s0 * M0HI;
+    uint32_t sp = (V & 2) ? t1 * p.shl : (t1 << p.L);
+    uint32_t s1 = ((hi ^ p.k[i] ^ t0) & p.LM) | sp;
+    t0 = s0;
+    t1 = s1;
+  }
+  return (t0 << p.R) | (t1 & p.RM);
+}
+
+template <int V>
+__device__ __forceinline__ uint32_t fwd(uint32_t x, const P& p) {
+  uint32_t s0 = x >> p.R, s1 = x & p.RM;
+#pragma unroll
+  for (int i = 0; i < 24; ++i) {
+    if (V == 8) {
+      uint32_t hi = __umulhi(s0, M0LO) + s0 * M0HI;
+      uint32_t lo = (s0 * (M0LO << 1)) | (s1 >> p.L);
+      s0 = (hi ^ p.k[i] ^ s1) & p.LM;
+      s1 = lo & p.RM;
+    } else if (V == 9) {
+      uint64_t w = (uint64_t)s0 * M0LO;
+      uint32_t hi = (uint32_t)(w >> 32) + s0 * M0HI;
+      uint32_t lo = (uint32_t)w * 2u + (s1 >> p.L);
+      s0 = (hi ^ p.k[i] ^ s1) & p.LM;
+      s1 = lo & p.RM;
+    } else {
+      uint64_t w = (uint64_t)s0 * M0LO;
+      uint32_t hi = (uint32_t)(w >> 32) + s0 * M0HI;
+      uint32_t lo = ((uint32_t)w << 1) | (s1 >> p.L);
+      s0 = (hi ^ p.k[i] ^ s1) & p.LM;
+      s1 = lo & p.RM;
+    }
+  }
+  return (s0 << p.R) | s1;
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) k(uint32_t n, P p, uint32_t* sink) {
+  uint32_t acc = 0;
+  for (uint32_t b = blockIdx.x * 1024 + threadIdx.x; b < n; b += gridDim.x * 1024) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc += (V >= 8) ? fwd<V>(b + j * 256, p) : inv<V>(b + j * 256, p);
+  }
+  if (acc == 0x1234567u) sink[0] = acc;
+}
+
+int main() {
+  P p; for (int i = 0; i < 24; ++i) p.k[i] = 0x9E3779B9u * (i + 7);
+  p.L = 14; p.R = 15; p.LM = (1u << 14) - 1; p.RM = (1u << 15) - 1; p.half = 0x80000000u; p.shl = 1u << 14;
+  uint32_t* sink; CK(cudaMalloc(&sink, 4));
+  cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  const uint32_t n = 1u << 29;
+  auto run = [&](auto kern, const char* name) {
+    kern<<<148 * 16, 256>>>(n, p, sink); kern<<<148 * 16, 256>>>(n, p, sink);
+    CK(cudaEventRecord(e0)); for (int r = 0; r < 5; ++r) kern<<<148 * 16, 256>>>(n, p, sink);
+    CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); ms /= 5;
+    printf("%-40s 2^29 inverse ciphers %7.3f ms  %7.1f G/s\n", name, ms, n / ms / 1e6);
+  };
+  run(k<0>, "SHF >>1, SHF <<L");
+  run(k<1>, "IMAD.HI >>1, SHF <<L");
+  run(k<2>, "SHF >>1, IMAD <<L");
+  run(k<3>, "IMAD.HI >>1, IMAD <<L");
+  run(k<6>, "inv: SHF >>1, IMAD <<L, WIDE hi");
+  run(k<8>, "fwd d1: HI, lo=IMAD|t (current)");
+  run(k<9>, "fwd d1: WIDE, lo=IMAD(wlo,2,t)");
+  run(k<10>, "fwd d1: WIDE, lo=(wlo<<1)|t");
+  return 0;
+}

@@ -1,0 +1,14 @@
+"""One shuffle of 2^bits u64 on the chosen path (for ncu launch lists)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2106_06161_b200 as bsg
+bits, path, variant = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 1
+m = 1 << bits
+vals = torch.arange(m, dtype=torch.int64, device="cuda")
+out = torch.empty_like(vals)
+bsg.set_path(path)
+cfg = bsg.ShuffleConfig(seed=0x5EED, variant=bsg.BijectionVariant(variant))
+for _ in range(2):
+    bsg.shuffle_values_into(vals, cfg, out)
+torch.cuda.synchronize()
