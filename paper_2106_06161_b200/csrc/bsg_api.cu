@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -87,7 +88,11 @@ struct DeviceCtx {
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
 int g_force_compact = 0;
-int g_path = 0;  // 0 auto, 1 single-pass only, 2 partitioned whenever eligible
+// 0 auto, 1 single-pass only, 2 partitioned whenever eligible; BSG_PATH overrides at load.
+int g_path = [] {
+  const char* e = std::getenv("BSG_PATH");
+  return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+}();
 // Auto mode uses the partitioned path for power-of-two shuffles whose payload
 // exceeds this many bytes (below it the single pass is L2-resident and faster).
 uint64_t g_partition_min_bytes = 256ULL << 20;

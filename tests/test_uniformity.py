@@ -1,0 +1,71 @@
+"""Statistical validation of the GPU shuffles (reference acceptance criteria 6
+and 7, proj/tests/acceptance.cpp:180-228), plus CPU checks of the helpers."""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import ensure_lib
+
+ensure_lib()
+import paper_2106_06161_b200 as bsg  # noqa: E402
+from paper_2106_06161_b200 import stats as S  # noqa: E402
+
+
+def test_permutation_rank_is_lexicographic():  # permutation.hpp:109-123
+    perms = torch.tensor(list(itertools.permutations(range(5))), dtype=torch.int64)
+    assert torch.equal(S.permutation_rank(perms), torch.arange(120))
+
+
+def test_kendall_distance_bruteforce():  # permutation.hpp:93-105 vs oracles.hpp brute force
+    rng = np.random.default_rng(1)
+    a = torch.from_numpy(np.stack([rng.permutation(40) for _ in range(30)]))
+    b = torch.from_numpy(np.stack([rng.permutation(40) for _ in range(30)]))
+    got = S.kendall_distance(a, b, chunk=7)
+    for i in range(30):
+        x, y = a[i].tolist(), b[i].tolist()  # slots ordered differently by the two one-line notations
+        brute = sum(1 for s, t in itertools.combinations(range(40), 2) if (x[s] - x[t]) * (y[s] - y[t]) < 0)
+        assert int(got[i]) == brute
+
+
+def test_mallows_moments_small_n():  # stats.hpp:41-62 vs enumeration over S_4
+    import math
+    n, lam = 4, 5.0
+    perms = torch.tensor(list(itertools.permutations(range(n))), dtype=torch.int64)
+    idp = torch.arange(n).expand_as(perms).contiguous()
+    d = S.kendall_distance(idp, perms).double()
+    k = (-lam * d / (n * (n - 1) / 2)).exp()
+    assert math.isclose(float(k.mean()), S.mallows_expectation(n, lam), rel_tol=1e-12)
+    assert math.isclose(float((k * k).mean() - k.mean() ** 2), S.mallows_variance(n, lam), rel_tol=1e-9)
+
+
+@pytest.mark.gpu
+def test_chi_squared_acceptance_criterion_6():
+    good = S.chi_squared_test(100000, bsg.ShuffleConfig(seed=0), 0.05)
+    bad = S.chi_squared_test(100000, bsg.ShuffleConfig(seed=0, variant=bsg.BijectionVariant.Lcg), 0.05)
+    assert good.passed, good
+    assert bad.statistic > 10 * bad.threshold, bad
+    # identical to the statistic of the CPU oracle's permutations (bit-exact samples)
+    ranks = np.zeros(120, dtype=np.int64)
+    fact = [24, 6, 2, 1, 1]
+    for b in range(100000):
+        p = O.shuffle_indices(5, b)
+        r = sum(int((p[i + 1:] < p[i]).sum()) * fact[i] for i in range(5))
+        ranks[r] += 1
+    exp = 100000 / 120
+    stat = float(((ranks - exp) ** 2 / exp).sum())
+    assert abs(stat - good.statistic) < 1e-9 * stat
+
+
+@pytest.mark.gpu
+def test_mmd_acceptance_criterion_7():
+    for n in (5, 100, 1000):
+        r = S.mmd_test(n, 10000, bsg.ShuffleConfig(seed=2), 0.05, S.TestKind.MmdNormal)
+        ident = torch.arange(n, device="cuda").repeat(10000, 1)
+        broken = S.mmd_test(n, 10000, None, 0.05, S.TestKind.MmdNormal, perms=ident)
+        assert r.passed, (n, r)
+        assert not broken.passed, (n, broken)

@@ -55,10 +55,17 @@ def launches(path: str):
     return out
 
 
-def raw_metrics(rep: str):
+def raw_metrics_all(rep: str):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    return [raw_metrics_row(rows[0], rows[1], r) for r in rows[2:]]
+
+
+def raw_metrics(rep: str):
+    return raw_metrics_all(rep)[0]
+
+
+def raw_metrics_row(hdr, units, vals):
     d = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
     res = {}
     for k in KEYS:
@@ -78,7 +85,7 @@ def raw_metrics(rep: str):
                 pass
     tot = sum(s for s, _ in stalls) or 1.0
     res["stall_pct"] = {n: round(100 * s / tot, 1) for s, n in sorted(stalls, reverse=True)[:8]}
-    res["kernel"] = short_name(d.get("Kernel Name", ("", ""))[0])
+    res["kernel"] = short_name(d.get("Kernel Name", ("", ""))[0]).replace("bsg::<unnamed>", "bsg")
     return res
 
 
@@ -103,7 +110,6 @@ def main():
           "`tools/ncu_summary.py`. Launch lists are cold-cache and serialised: compare shares, not absolutes.", ""]
     for cfg in args.configs.split(","):
         lp = os.path.join(args.src, f"launches_{cfg}.csv")
-        rp = os.path.join(args.src, f"prof_{cfg}.ncu-rep")
         if os.path.exists(lp):
             L = launches(lp)
             with open(os.path.join(prof, f"{args.round}_launches_{cfg}.csv"), "w", newline="") as f:
@@ -121,21 +127,28 @@ def main():
             for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
                 md.append(f"| `{k}` | {n} | {ns / 1e6:.3f} | {100 * ns / tot:.1f}% |")
             md.append("")
-        if os.path.exists(rp):
-            R = raw_metrics(rp)
-            with open(os.path.join(prof, f"{args.round}_ncu_{cfg}.json"), "w") as f:
-                json.dump(R, f, indent=1)
-            rd = to_bytes(R["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in R else None
-            wr = to_bytes(R["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in R else None
-            if rd is not None and wr is not None:
-                traffic[cfg] = {"kernel": R["kernel"], "dram_bytes_per_launch": rd + wr, "dram_read": rd,
-                                "dram_write": wr, "source": f"profiles/{args.round}_ncu_{cfg}.json"}
-            md += [f"## {cfg}: `{R['kernel']}` full-set capture", "", "| metric | value |", "|---|---:|"]
-            for k in KEYS:
-                if k in R:
-                    md.append(f"| `{k}` | {R[k]['value']} {R[k]['unit']} |")
-            md.append(f"| warp stall mix (pc sampling) | {', '.join(f'{k} {v}%' for k, v in R['stall_pct'].items())} |")
-            md.append("")
+        for suffix in ("", "single"):
+            rp = os.path.join(args.src, f"prof_{cfg}{suffix}.ncu-rep")
+            if not os.path.exists(rp):
+                continue
+            RS = raw_metrics_all(rp)
+            with open(os.path.join(prof, f"{args.round}_ncu_{cfg}{suffix}.json"), "w") as f:
+                json.dump(RS, f, indent=1)
+            rd = sum(to_bytes(R["dram__bytes_read.sum"]) for R in RS if "dram__bytes_read.sum" in R)
+            wr = sum(to_bytes(R["dram__bytes_write.sum"]) for R in RS if "dram__bytes_write.sum" in R)
+            names = "+".join(R["kernel"] for R in RS)
+            key = cfg + (f"_{suffix}" if suffix else "")
+            traffic[key] = {"kernel": names, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                            "source": f"profiles/{args.round}_ncu_{cfg}{suffix}.json",
+                            "note": "sum over the kernels of one shuffle" if len(RS) > 1 else "one launch"}
+            for R in RS:
+                md += [f"## {key}: `{R['kernel']}` full-set capture", "", "| metric | value |", "|---|---:|"]
+                for k in KEYS:
+                    if k in R:
+                        md.append(f"| `{k}` | {R[k]['value']} {R[k]['unit']} |")
+                md.append(f"| warp stall mix (pc sampling) | "
+                          f"{', '.join(f'{k} {v}%' for k, v in R['stall_pct'].items())} |")
+                md.append("")
     with open(traffic_path, "w") as f:
         json.dump(traffic, f, indent=1)
     with open(os.path.join(prof, f"{args.round}_summary.md"), "w") as f:
