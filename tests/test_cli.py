@@ -55,7 +55,7 @@ def test_cli_shuffle_and_test_and_bench():
     assert good.returncode == 0 and json.loads(good.stdout)["pass"] is True
     bad = cli("test", "--kind", "chi2", "--gen", "lcg", "--samples", "100000")
     assert bad.returncode == 1 and json.loads(bad.stdout)["pass"] is False
-    fy = cli("test", "--kind", "mmd-normal", "--gen", "fisher-yates", "--n", "100", "--samples", "2000")
+    fy = cli("test", "--kind", "mmd-normal", "--gen", "fisher-yates", "--n", "100", "--samples", "10000")  # acceptance.cpp:347-349
     assert fy.returncode == 0, fy.stdout + fy.stderr
     b = cli("bench", "--sizes", "1025,65537", "--trials", "2")
     assert b.returncode == 0
