@@ -138,6 +138,22 @@ bsg_status bsg_dist_shuffle_values(uint64_t m, const bsg_config* cfg, int32_t ra
 /* Counter range [begin, end) owned by `rank` of `world` for an m-element shuffle. */
 bsg_status bsg_dist_counter_range(uint64_t m, int32_t rank, int32_t world, uint64_t* begin, uint64_t* end);
 
+/* Sharded power-of-two shuffle by destination routing: the
+ * local elements global_offset .. global_offset+n_local-1 of an m-element
+ * shuffle (m = 2^bits <= 2^32) are grouped by the part owning their output
+ * position f^-1(j) (nparts contiguous output shards of m/nparts); out_dest
+ * holds the position inside the part; part_counts (host, nparts) the group
+ * sizes.  An all-to-all of the groups followed by bsg_scatter_permutation on
+ * each part completes the shuffle with bulk transfers only.  Device pointers. */
+bsg_status bsg_route_by_dest(const void* in, uint64_t n_local, uint64_t global_offset, uint64_t m,
+                             const bsg_config* cfg, int32_t nparts, void* out_values, uint32_t* out_dest,
+                             uint64_t* part_counts, uint32_t elem_bytes, void* stream);
+/* out[dest[i]] = values[i] where dest is a permutation of [0, n): the
+ * partitioned three-pass placement for large power-of-two n, a direct scatter
+ * otherwise.  elem_bytes 4, 8 or 16; device pointers. */
+bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uint64_t n, void* out,
+                                   uint32_t elem_bytes, void* stream);
+
 /* CUDA IPC helpers for sharded inputs across processes (one process per GPU). */
 #define BSG_IPC_HANDLE_BYTES 64
 bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_HANDLE_BYTES]);

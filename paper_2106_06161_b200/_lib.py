@@ -52,6 +52,9 @@ SIGNATURES = {
                                           POINTER(bsg_shards), c_void_p, c_uint32, ALLGATHER_FN, c_void_p,
                                           POINTER(c_uint64), POINTER(c_uint64), c_void_p]),
     "bsg_dist_counter_range": (c_int32, [c_uint64, c_int32, c_int32, POINTER(c_uint64), POINTER(c_uint64)]),
+    "bsg_route_by_dest": (c_int32, [c_void_p, c_uint64, c_uint64, c_uint64, POINTER(bsg_config), c_int32, c_void_p,
+                                    c_void_p, POINTER(c_uint64), c_uint32, c_void_p]),
+    "bsg_scatter_permutation": (c_int32, [c_void_p, c_void_p, c_uint64, c_void_p, c_uint32, c_void_p]),
     "bsg_ipc_export": (c_int32, [c_void_p, POINTER(c_ubyte)]),
     "bsg_ipc_open": (c_int32, [POINTER(c_ubyte), POINTER(c_void_p)]),
     "bsg_ipc_close": (c_int32, [c_void_p]),

@@ -648,6 +648,89 @@ bsg_status bsg_dist_shuffle_values(uint64_t m, const bsg_config* cfg_in, int32_t
   return BSG_OK;
 }
 
+bsg_status bsg_route_by_dest(const void* in, uint64_t n_local, uint64_t global_offset, uint64_t m,
+                             const bsg_config* cfg_in, int32_t nparts, void* out_values, uint32_t* out_dest,
+                             uint64_t* part_counts, uint32_t elem_bytes, void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (m < 16 || (m & (m - 1))) return fail(BSG_EINVAL, "route_by_dest: m must be a power of two >= 16");
+  const int bits = bsg::domain_bits(m);
+  if (bits > 32) return fail(BSG_EUNSUPPORTED, "route_by_dest: m <= 2^32");
+  if (nparts < 1 || nparts > 64 || (nparts & (nparts - 1)) || m % static_cast<uint64_t>(nparts))
+    return fail(BSG_EINVAL, "route_by_dest: nparts must be a power of two <= 64 dividing m");
+  if (global_offset > m || n_local > m - global_offset) return fail(BSG_ERANGE, "route_by_dest: local range outside m");
+  if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16)
+    return fail(BSG_EUNSUPPORTED, "route_by_dest: elem_bytes must be 4, 8 or 16");
+  BijParams p;
+  BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, p));
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (!is_device_ptr(in) || !is_device_ptr(out_values) || !is_device_ptr(out_dest))
+      return fail(BSG_EINVAL, "route_by_dest: device pointers only");
+    BSG_CUDA(c->st_idx.ensure(std::max<uint64_t>(n_local, 1) * 4 + 2 * 64 * 8));
+    char* w = static_cast<char*>(c->st_idx.p);
+    bsg::RouteLaunch R;
+    R.in = in;
+    R.n = n_local;
+    R.offset = global_offset;
+    R.part_size = m / nparts;
+    R.nparts = nparts;
+    R.p = p;
+    R.counts = reinterpret_cast<unsigned long long*>(w);
+    R.cursors = reinterpret_cast<unsigned long long*>(w + 64 * 8);
+    R.tmp_dest = reinterpret_cast<uint32_t*>(w + 2 * 64 * 8);
+    R.out_values = out_values;
+    R.out_dest = out_dest;
+    BSG_TRY(ws_begin(c, s));
+    BSG_TRY(upload_keys(c, R.p, cfg.seed, s));
+    if (n_local) BSG_CUDA(bsg::launch_route(static_cast<int>(elem_bytes), R, s));
+    else BSG_CUDA(cudaMemsetAsync(R.counts, 0, 64 * 8, s));
+    BSG_TRY(ws_end(c, s));
+    if (part_counts) {
+      BSG_CUDA(cudaMemcpyAsync(part_counts, R.counts, sizeof(uint64_t) * nparts, cudaMemcpyDeviceToHost, s));
+      BSG_CUDA(cudaStreamSynchronize(s));
+    }
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uint64_t n, void* out,
+                                   uint32_t elem_bytes, void* stream) {
+  if (n == 0) return BSG_OK;
+  if (values == out) return fail(BSG_EALIAS, "scatter_permutation: out aliases input");
+  if (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16)
+    return fail(BSG_EUNSUPPORTED, "scatter_permutation: elem_bytes must be 4, 8 or 16");
+  if (n > (1ULL << 32)) return fail(BSG_EUNSUPPORTED, "scatter_permutation: n <= 2^32");
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (!is_device_ptr(values) || !is_device_ptr(dest) || !is_device_ptr(out))
+      return fail(BSG_EINVAL, "scatter_permutation: device pointers only");
+    const int code = static_cast<int>(elem_bytes);
+    int bits = 0;
+    while ((1ULL << bits) < n) ++bits;
+    BSG_TRY(ws_begin(c, s));
+    const bool pow2 = (1ULL << bits) == n;
+    if (pow2 && g_path != 1 && bsg::partition_eligible(code, bits) &&
+        (g_path == 2 || n * static_cast<uint64_t>(elem_bytes) >= g_partition_min_bytes) &&
+        c->part.ensure(bsg::partition_workspace_bytes(code, bits)) == cudaSuccess) {
+      char* w = static_cast<char*>(c->part.p);
+      bsg::PartitionLaunch P;
+      P.in = values;
+      P.out = out;
+      P.tmp_values = w;
+      P.tmp_dest = reinterpret_cast<uint32_t*>(w + n * elem_bytes);
+      P.tmp_dlow = reinterpret_cast<uint16_t*>(w + n * elem_bytes + n * 4);
+      P.cursors = reinterpret_cast<uint32_t*>(w + n * elem_bytes + n * 6);
+      P.dest_in = dest;
+      P.p.bits = bits;
+      BSG_CUDA(bsg::launch_partition(code, P, s));
+    } else {
+      cudaGetLastError();
+      BSG_CUDA(bsg::launch_scatter_simple(code, values, dest, n, out, s));
+    }
+    return ws_end(c, s);
+  });
+}
+
 bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_HANDLE_BYTES]) {
   cudaIpcMemHandle_t h;
   BSG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));

@@ -41,6 +41,8 @@ constexpr int kP2Threads = BSG_P2_THREADS, kP2Items = 4096 / BSG_P2_THREADS, kP2
 constexpr int kP3Threads = 512;
 constexpr int kMaxB1 = 512, kMaxB2 = 256;
 
+constexpr int kKindDestArray = 100;  // destinations come from an array (scatter by permutation)
+
 template <int KIND, int D>
 __device__ __forceinline__ uint32_t inv_bij(uint32_t y, const BijParams& p) {
   if constexpr (KIND == kKindLcg) return static_cast<uint32_t>(lcg_inv(y, p));
@@ -91,7 +93,8 @@ __device__ __forceinline__ void scan_bins(const uint32_t* hist, uint32_t* start,
 template <int KIND, int D, typename T>
 __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, T* __restrict__ tv,
                                                          uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
-                                                         BijParams p, int bshift, int nb, uint64_t w1) {
+                                                         BijParams p, int bshift, int nb, uint64_t w1,
+                                                         const uint32_t* __restrict__ dsrc) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
   uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);
@@ -106,7 +109,8 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
   uint32_t dst[kP1Items], rk[kP1Items];
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
-    dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
+    if constexpr (KIND == kKindDestArray) dst[i] = __ldcs(dsrc + base + i * kP1Threads);
+    else dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
     rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
   }
   __syncthreads();
@@ -233,7 +237,7 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
   T* tv = static_cast<T*>(a.tmp_values);
   k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
-      static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1);
+      static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in);
   k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
                                                                           a.tmp_dlow, cur2, w2, nb2, w1);
   k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2);
@@ -243,6 +247,7 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
 
 template <typename T>
 cudaError_t dispatch_partition(const PartitionLaunch& a, cudaStream_t s) {
+  if (a.dest_in) return run_partition<kKindDestArray, 0, T>(a, s);
   switch (kind_of(a.p)) {
     case kKindLcg: return run_partition<kKindLcg, 0, T>(a, s);
     case kKindPh0: return run_partition<kKindPh0, 0, T>(a, s);
@@ -253,7 +258,163 @@ cudaError_t dispatch_partition(const PartitionLaunch& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+
+// ------------------------------------------------------------------------
+// Route-by-destination (multi-GPU sharded power-of-two shuffle):
+// for local elements j = offset + i, dest = f^-1(j); group them by the rank
+// owning dest (contiguous output shards of `part_size`), keeping the
+// destination inside the part.  Two kernels: destinations + part histogram,
+// then a tiled counting sort into the part groups.
+template <int KIND, int D>
+__global__ void __launch_bounds__(256) k_route_dest(uint64_t n, uint64_t offset, BijParams p, int part_shift,
+                                                    int nparts, uint32_t* __restrict__ dest,
+                                                    unsigned long long* __restrict__ counts) {
+  __shared__ uint32_t h[64];
+  if (threadIdx.x < 64) h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t d = inv_bij<KIND, D>(static_cast<uint32_t>(offset + i), p);
+    dest[i] = d;
+    atomicAdd(&h[d >> part_shift], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < nparts && h[threadIdx.x]) atomicAdd(counts + threadIdx.x, static_cast<unsigned long long>(h[threadIdx.x]));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kP2Threads) k_route(const T* __restrict__ in, const uint32_t* __restrict__ dest,
+                                                      uint64_t n, int part_shift, int nparts,
+                                                      unsigned long long* __restrict__ cursors, T* __restrict__ ov,
+                                                      uint32_t* __restrict__ od) {
+  __shared__ uint32_t hist[64], start[64], wt[32];
+  __shared__ unsigned long long gbase[64];
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sv = reinterpret_cast<T*>(smem);
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
+  const int tid = threadIdx.x;
+  if (tid < 64) hist[tid] = 0;
+  __syncthreads();
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kP2Tile;
+  T v[kP2Items];
+  uint32_t d[kP2Items], rk[kP2Items];
+#pragma unroll
+  for (int i = 0; i < kP2Items; ++i) {
+    const uint64_t e = t0 + tid + i * kP2Threads;
+    if (e < n) {
+      v[i] = __ldcs(in + e);
+      d[i] = __ldcs(dest + e);
+      rk[i] = atomicAdd(&hist[d[i] >> part_shift], 1u);
+    }
+  }
+  __syncthreads();
+  scan_bins(hist, start, nparts, wt);
+  if (tid < nparts) gbase[tid] = atomicAdd(cursors + tid, static_cast<unsigned long long>(hist[tid]));
+  __syncthreads();
+  const uint32_t mask = (part_shift >= 32) ? 0xFFFFFFFFu : ((1u << part_shift) - 1);
+#pragma unroll
+  for (int i = 0; i < kP2Items; ++i) {
+    if (t0 + tid + i * kP2Threads < n) {
+      const uint32_t s = start[d[i] >> part_shift] + rk[i];
+      sv[s] = v[i];
+      sd[s] = d[i];
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = static_cast<uint32_t>(n - t0 < kP2Tile ? n - t0 : kP2Tile);
+  for (uint32_t s = tid; s < cnt; s += kP2Threads) {
+    const uint32_t dd = sd[s], b = dd >> part_shift;
+    const uint64_t pos = gbase[b] + (s - start[b]);
+    __stcs(ov + pos, sv[s]);
+    __stcs(od + pos, dd & mask);
+  }
+}
+
+template <int KIND, int D, typename T>
+cudaError_t run_route(const RouteLaunch& a, cudaStream_t s) {
+  int shift = 0;
+  while ((1ULL << shift) < a.part_size) ++shift;
+  cudaError_t e = cudaMemsetAsync(a.counts, 0, sizeof(unsigned long long) * a.nparts, s);
+  if (e != cudaSuccess) return e;
+  const uint64_t blocks = (a.n + 255) / 256;
+  k_route_dest<KIND, D><<<static_cast<unsigned>(blocks < 148ull * 16 ? blocks : 148ull * 16), 256, 0, s>>>(
+      a.n, a.offset, a.p, shift, a.nparts, a.tmp_dest, a.counts);
+  // exclusive prefix of the part counts -> cursors (nparts <= 64: one tiny kernel-free step on the host side
+  // would force a sync; do it on the device instead)
+  e = launch_exclusive_prefix_u64(a.counts, a.cursors, a.nparts, s);
+  if (e != cudaSuccess) return e;
+  const size_t sm = kP2Tile * (sizeof(T) + 4);
+  cudaFuncSetAttribute(k_route<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  k_route<T><<<static_cast<unsigned>((a.n + kP2Tile - 1) / kP2Tile), kP2Threads, sm, s>>>(
+      static_cast<const T*>(a.in), a.tmp_dest, a.n, shift, a.nparts, a.cursors, static_cast<T*>(a.out_values),
+      a.out_dest);
+  note_launch(3);
+  return cudaGetLastError();
+}
+
+__global__ void k_excl_prefix(const unsigned long long* c, unsigned long long* o, int n) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long r = 0;
+    for (int i = 0; i < n; ++i) {
+      o[i] = r;
+      r += c[i];
+    }
+  }
+}
+
+template <typename T>
+cudaError_t dispatch_route(const RouteLaunch& a, cudaStream_t s) {
+  switch (kind_of(a.p)) {
+    case kKindLcg: return run_route<kKindLcg, 0, T>(a, s);
+    case kKindPh0: return run_route<kKindPh0, 0, T>(a, s);
+    case kKindPh1: return run_route<kKindPh1, 1, T>(a, s);
+    case kKindPh0G: return run_route<kKindPh0G, 0, T>(a, s);
+    case kKindPh1G: return run_route<kKindPh1G, 1, T>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+template <typename T>
+__global__ void k_scatter_simple(const T* __restrict__ in, const uint32_t* __restrict__ dest, uint64_t n,
+                                 T* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[dest[i]] = in[i];
+}
+
+template <typename T>
+cudaError_t scatter_simple(const void* in, const uint32_t* dest, uint64_t n, void* out, cudaStream_t s) {
+  const uint64_t blocks = (n + 255) / 256;
+  k_scatter_simple<T><<<static_cast<unsigned>(blocks < 148ull * 32 ? blocks : 148ull * 32), 256, 0, s>>>(
+      static_cast<const T*>(in), dest, n, static_cast<T*>(out));
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t launch_scatter_simple(int elem_code, const void* in, const uint32_t* dest, uint64_t n, void* out,
+                                  cudaStream_t s) {
+  switch (elem_code) {
+    case 4: return scatter_simple<uint32_t>(in, dest, n, out, s);
+    case 8: return scatter_simple<uint64_t>(in, dest, n, out, s);
+    case 16: return scatter_simple<uint4>(in, dest, n, out, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_exclusive_prefix_u64(const unsigned long long* c, unsigned long long* o, int n, cudaStream_t s) {
+  k_excl_prefix<<<1, 32, 0, s>>>(c, o, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route(int elem_code, const RouteLaunch& a, cudaStream_t s) {
+  switch (elem_code) {
+    case 4: return dispatch_route<uint32_t>(a, s);
+    case 8: return dispatch_route<uint64_t>(a, s);
+    case 16: return dispatch_route<uint4>(a, s);
+  }
+  return cudaErrorNotSupported;
+}
 
 bool partition_eligible(int elem_code, int bits) {
   int w2;

@@ -13,8 +13,27 @@ struct PartitionLaunch {
   uint32_t* tmp_dest = nullptr;  // n u32 destinations
   uint16_t* tmp_dlow = nullptr;  // n u16 destinations inside a fine window
   uint32_t* cursors = nullptr;   // bucket append cursors
+  const uint32_t* dest_in = nullptr;  // given destinations (scatter by permutation) instead of f^-1
   BijParams p;
 };
+
+struct RouteLaunch {
+  const void* in = nullptr;       // n local elements, global indices offset .. offset+n-1
+  uint64_t n = 0, offset = 0;
+  uint64_t part_size = 0;         // output shard size (power of two)
+  int nparts = 0;                 // <= 64
+  BijParams p;
+  uint32_t* tmp_dest = nullptr;   // n
+  unsigned long long* counts = nullptr;   // nparts (device)
+  unsigned long long* cursors = nullptr;  // nparts (device)
+  void* out_values = nullptr;     // n, grouped by part
+  uint32_t* out_dest = nullptr;   // n, destination inside the part
+};
+
+cudaError_t launch_scatter_simple(int elem_code, const void* in, const uint32_t* dest, uint64_t n, void* out,
+                                  cudaStream_t s);
+cudaError_t launch_route(int elem_code, const RouteLaunch& a, cudaStream_t s);
+cudaError_t launch_exclusive_prefix_u64(const unsigned long long* c, unsigned long long* o, int n, cudaStream_t s);
 
 bool partition_eligible(int elem_code, int bits);
 size_t partition_workspace_bytes(int elem_code, int bits);

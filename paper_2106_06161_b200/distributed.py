@@ -123,6 +123,55 @@ def rebalance(piece, counts: Sequence[int], m: int, group=None):
     return out
 
 
+def _gpu_route(local, m, cfg, rank, world):
+    import torch
+    S = local.numel()
+    vals = torch.empty_like(local)
+    dl = torch.empty(S, dtype=torch.int32, device=local.device)
+    counts = (ctypes.c_uint64 * world)()
+    stream = torch.cuda.current_stream(local.device).cuda_stream
+    check(lib.bsg_route_by_dest(local.data_ptr(), S, rank * S, m, ctypes.byref(cfg._c()), world, vals.data_ptr(),
+                                dl.data_ptr(), counts, local.element_size(), stream), "route_by_dest")
+    return vals, dl, [int(c) for c in counts]
+
+
+def _gpu_scatter(vals, dest, n):
+    import torch
+    out = torch.empty(n, dtype=vals.dtype, device=vals.device)
+    stream = torch.cuda.current_stream(vals.device).cuda_stream
+    check(lib.bsg_scatter_permutation(vals.data_ptr(), dest.data_ptr(), n, out.data_ptr(), vals.element_size(),
+                                      stream), "scatter_permutation")
+    return out
+
+
+def shuffle_values_sharded(local_shard, m: int, cfg: Optional[ShuffleConfig] = None, group=None,
+                           route_fn: Optional[Callable] = None, scatter_fn: Optional[Callable] = None):
+    """Power-of-two shuffle of an input sharded in `world` equal contiguous pieces; returns this rank's
+    equal output shard out[rank*S:(rank+1)*S].  Bulk transfers only:
+    route local elements by destination rank (f^-1, bsg_route_by_dest), one NCCL all-to-all of the
+    groups (values and in-shard destinations), then place them (bsg_scatter_permutation)."""
+    import torch
+    import torch.distributed as dist
+    cfg = cfg or ShuffleConfig()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if m & (m - 1) or m % world or local_shard.numel() != m // world:
+        raise _lib.InvalidArgument("sharded shuffle: m must be a power of two split evenly over the ranks")
+    S = m // world
+    vals, dl, send = (route_fn or _gpu_route)(local_shard, m, cfg, rank, world)
+    dev = local_shard.device
+    sc = torch.tensor(send, dtype=torch.int64, device=dev)
+    rc = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(rc, sc, group=group)  # group sizes
+    recv = [int(x) for x in rc.tolist()]
+    if sum(recv) != S:
+        raise _lib.CudaError(f"sharded shuffle: received {sum(recv)} elements for a shard of {S}")
+    rv = torch.empty(S, dtype=vals.dtype, device=dev)
+    rd = torch.empty(S, dtype=dl.dtype, device=dev)
+    dist.all_to_all_single(rv, vals, output_split_sizes=recv, input_split_sizes=send, group=group)
+    dist.all_to_all_single(rd, dl, output_split_sizes=recv, input_split_sizes=send, group=group)
+    return (scatter_fn or _gpu_scatter)(rv, rd, S)
+
+
 def ipc_shards(local_shard, group=None) -> "_lib.bsg_shards":
     """Exchange CUDA IPC handles of each rank's equally sized input shard and map every peer's shard
     (NVLink peer reads).  Returns the bsg_shards table for `shuffle_values(..., shards=...)`."""

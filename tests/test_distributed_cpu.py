@@ -75,3 +75,59 @@ def test_distributed_equals_single(world, m, variant, orc):
     assert np.array_equal(shards, exp)
     sizes = [len(r[4]) for r in res]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _sharded_worker(rank, world, port, m, seed, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+
+    import oracle as O
+    import paper_2106_06161_b200 as bsg
+    from paper_2106_06161_b200 import distributed as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bits = m.bit_length() - 1
+
+        def route(local, m_, cfg, r, w):  # oracle stand-in for bsg_route_by_dest
+            S = local.numel()
+            dest = np.array([O.philox_invert(bits, cfg.seed, cfg.num_rounds, r * S + i) for i in range(S)],
+                            dtype=np.int64)
+            part = dest // (m_ // w)
+            order = np.argsort(part, kind="stable")
+            counts = [int((part == p).sum()) for p in range(w)]
+            return (local[torch.from_numpy(order)], torch.from_numpy((dest % (m_ // w))[order]).to(torch.int32),
+                    counts)
+
+        def scatter(vals, dest, n):  # oracle stand-in for bsg_scatter_permutation
+            out = torch.empty(n, dtype=vals.dtype)
+            out[dest.long()] = vals
+            return out
+
+        S = m // world
+        local = torch.arange(rank * S, (rank + 1) * S, dtype=torch.int64) * 3
+        out = D.shuffle_values_sharded(local, m, bsg.ShuffleConfig(seed=seed), route_fn=route, scatter_fn=scatter)
+        q.put((rank, out.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_by_destination_equals_single(world, orc):
+    ensure_lib()
+    m = 1 << 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, m, 77, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = np.concatenate([r[1] for r in res]).view(np.uint64)
+    exp = orc.shuffle_values(np.arange(m, dtype=np.uint64) * 3, 77, 1, 24)
+    assert np.array_equal(full, exp)

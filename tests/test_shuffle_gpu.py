@@ -414,3 +414,41 @@ def test_partitioned_path_matches_single_pass(bsg, cuda, golden):
     finally:
         bsg.set_path(old)
         cuda.cuda.empty_cache()
+
+
+def test_route_and_scatter_sharded_simulation(bsg, cuda):
+    """Sharded pow2 shuffle by destination routing, every rank simulated in one process:
+    route (bsg_route_by_dest) -> exchange (slicing, as the all-to-all would) -> place (bsg_scatter_permutation)."""
+    from paper_2106_06161_b200 import distributed as D
+    for m, W, dt in (((1 << 20), 4, cuda.int64), ((1 << 22), 8, cuda.int32), ((1 << 16), 2, cuda.int64)):
+        cfg = cfg_of(bsg, seed=m + W)
+        S = m // W
+        full_in = cuda.arange(m, dtype=dt, device="cuda") * 5 + 1
+        routed = [D._gpu_route(full_in[r * S:(r + 1) * S].contiguous(), m, cfg, r, W) for r in range(W)]
+        out = []
+        for dst in range(W):
+            vs, ds = [], []
+            for src in range(W):
+                vals, dl, counts = routed[src]
+                off = sum(counts[:dst])
+                vs.append(vals[off:off + counts[dst]])
+                ds.append(dl[off:off + counts[dst]])
+            out.append(D._gpu_scatter(cuda.cat(vs), cuda.cat(ds), S))
+        got = cuda.cat(out)
+        exp = bsg.shuffle_values(full_in, cfg)
+        assert cuda.equal(got, exp), (m, W)
+
+
+def test_scatter_permutation_paths(bsg, cuda):
+    from paper_2106_06161_b200 import distributed as D
+    for n, path in ((1 << 12, 0), (1 << 21, 2), (1 << 21, 1)):
+        old = bsg.set_path(path)
+        try:
+            perm = bsg.shuffle_indices(n, cfg_of(bsg, seed=n), device="cuda")
+            vals = cuda.arange(n, dtype=cuda.int64, device="cuda")
+            out = D._gpu_scatter(vals, perm.to(cuda.int32), n)
+            ref = cuda.empty_like(vals)
+            ref[perm] = vals
+            assert cuda.equal(out, ref), (n, path)
+        finally:
+            bsg.set_path(old)
