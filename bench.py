@@ -319,15 +319,21 @@ def ours_arm(args, rank, world, local):
                     "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call"}
             del pairs
         else:
-            host_in = torch.arange(m_total, dtype=tdt).pin_memory()
-            host_out = torch.empty(out.numel(), dtype=tdt).pin_memory()
+            # Distributed data: each rank's host holds one input shard; the global power-of-two shuffle is
+            # routed by destination (bsg_route_by_dest), exchanged with one NCCL all-to-all and placed
+            # (bsg_scatter_permutation); each rank reads back its output shard.
+            from paper_2106_06161_b200 import distributed as D
+            S = m_total // world
+            host_in = (torch.arange(rank * S, (rank + 1) * S, dtype=tdt)).pin_memory()
+            host_out = torch.empty(S, dtype=tdt).pin_memory()
+            dev_in = torch.empty(S, dtype=tdt, device=dev)
 
             def e2e_step():
-                vals.copy_(host_in, non_blocking=True)
-                step()
-                host_out.copy_(out, non_blocking=True)
+                dev_in.copy_(host_in, non_blocking=True)
+                res = D.shuffle_values_sharded(dev_in, m_total, cfg)
+                host_out.copy_(res, non_blocking=True)
                 torch.cuda.current_stream(dev).synchronize()
-            h2d, d2h = m_total * eb, out.numel() * eb
+            h2d, d2h = S * eb, S * eb
             e2e_step()
             barrier()
             t0 = time.perf_counter()
@@ -335,9 +341,10 @@ def ours_arm(args, rank, world, local):
                 e2e_step()
             barrier()
             el = time.perf_counter() - t0
-            path = "per rank: H2D of the replicated input, shuffle_range + count allgather, D2H of the rank's piece"
+            path = ("per rank: H2D of its input shard, route by destination, NCCL all-to-all, place, "
+                    "D2H of its output shard (distributed.shuffle_values_sharded)")
             sync = None
-            del host_in, host_out
+            del host_in, host_out, dev_in
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([el], device=dev)

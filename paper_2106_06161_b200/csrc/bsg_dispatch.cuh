@@ -64,13 +64,17 @@ cudaError_t dispatch_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
 
 template <int KIND, typename T>
 cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(a.m) * sizeof(T);
+  const size_t row_bytes = static_cast<size_t>(a.m) * sizeof(T);
+  const size_t stride = (row_bytes + 15) / 16 * 16;
+  const size_t smem = 2 * stride;  // double-buffered rows
+  int mode = 0;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(a.in);
+  if (row_bytes % 16 == 0 && base % 16 == 0) mode = 1;
+  else if (row_bytes % 4 == 0 && base % 4 == 0) mode = 2;
   auto kern = k_batched<KIND, T>;
-  static thread_local size_t configured = 0;  // per instantiation: raised opt-in limit
-  if (smem > 48 * 1024 && configured < smem) {
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -79,7 +83,8 @@ cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
   if (per_sm < 1) return cudaErrorNotSupported;
   const uint64_t want = static_cast<uint64_t>(sms) * per_sm;
   const unsigned grid = static_cast<unsigned>(a.batch < want ? a.batch : want);
-  kern<<<grid, kThreads, smem, s>>>(static_cast<const T*>(a.in), static_cast<T*>(a.out), a.batch, a.m, a.seed, a.p);
+  kern<<<grid, kThreads, smem, s>>>(static_cast<const T*>(a.in), static_cast<T*>(a.out), a.batch, a.m, a.seed, a.p,
+                                    mode, static_cast<uint32_t>(stride));
   note_launch();
   return cudaGetLastError();
 }

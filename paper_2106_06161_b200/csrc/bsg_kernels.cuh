@@ -433,12 +433,17 @@ __device__ __forceinline__ uint32_t philox_keys_fwd(uint32_t x, const uint32_t* 
   return (s0 << R) | (s1 & RM);
 }
 
+// Rows are double-buffered in shared memory: while shuffle b is evaluated, the
+// row of the CTA's next shuffle streams in with cp.async and its round keys
+// are derived by the first `rounds` threads, so neither the load latency nor
+// the key schedule serialises with the cipher.
+// row_mode: 1 = 16-byte cp.async chunks, 2 = 4-byte chunks, 0 = plain loads.
 template <int KIND, typename T>
 __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, T* __restrict__ out, uint64_t batch,
-                                                      uint32_t m, uint64_t seed, BijParams p) {
+                                                      uint32_t m, uint64_t seed, BijParams p, int row_mode,
+                                                      uint32_t row_stride_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* s_row = reinterpret_cast<T*>(smem_raw);
-  __shared__ uint32_t s_keys[kBatchedMaxRounds];
+  __shared__ uint32_t s_keys[2][kBatchedMaxRounds];
   __shared__ uint32_t s_wcnt[2][kWarps];
   constexpr bool kFast = (KIND == kKindPh0 || KIND == kKindPh1);
   constexpr int D = (KIND == kKindPh1 || KIND == kKindPh1G) ? 1 : 0;
@@ -446,17 +451,55 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
   const uint32_t n = 1u << p.bits;
   const uint32_t mask32 = n - 1;
   const bool pow2 = (m == n);
-  for (uint64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    const uint64_t sb = seed + b;
-    if (KIND != kKindLcg && tid < p.rounds) s_keys[tid] = round_key(sb, tid);
-    const T* row_in = in + b * m;
-    T* row_out = out + b * m;
-    for (uint32_t i = tid; i < m; i += kThreads) s_row[i] = row_in[i];
+  const uint32_t row_bytes = m * static_cast<uint32_t>(sizeof(T));
+
+  auto row_ptr = [&](int buf) { return reinterpret_cast<T*>(smem_raw + buf * row_stride_bytes); };
+  auto issue_row = [&](uint64_t b, int buf) {
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(in + b * m);
+    unsigned char* dst = smem_raw + buf * row_stride_bytes;
+    if (row_mode == 1) {
+      for (uint32_t o = tid * 16; o < row_bytes; o += kThreads * 16) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + o));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + o) : "memory");
+      }
+    } else if (row_mode == 2) {
+      for (uint32_t o = tid * 4; o < row_bytes; o += kThreads * 4) {
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + o));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + o) : "memory");
+      }
+    } else {
+      T* r = reinterpret_cast<T*>(dst);
+      for (uint32_t i = tid; i < m; i += kThreads) r[i] = in[b * m + i];
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto make_keys = [&](uint64_t b, int buf) {
+    if (KIND != kKindLcg && tid < p.rounds) s_keys[buf][tid] = round_key(seed + b, tid);
+  };
+
+  int buf = 0;
+  if (blockIdx.x < batch) {
+    issue_row(blockIdx.x, 0);
+    make_keys(blockIdx.x, 0);
+  }
+  for (uint64_t b = blockIdx.x; b < batch; b += gridDim.x, buf ^= 1) {
+    const uint64_t nb = b + gridDim.x;
+    if (nb < batch) {
+      issue_row(nb, buf ^ 1);
+      make_keys(nb, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
+    const T* s_row = row_ptr(buf);
+    const uint32_t* keys = s_keys[buf];
+    T* row_out = out + b * m;
+    const uint64_t sb = seed + b;
     uint32_t kr[kFast ? 24 : 1];
     if constexpr (kFast) {
 #pragma unroll
-      for (int i = 0; i < 24; ++i) kr[i] = s_keys[i];
+      for (int i = 0; i < 24; ++i) kr[i] = keys[i];
     }
     // LCG parameters of this shuffle (make_lcg, bijection.hpp:25-34)
     const uint32_t la = static_cast<uint32_t>((mix64(sb) | 1ULL)) & mask32;
@@ -464,33 +507,34 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
     auto f = [&](uint32_t c) -> uint32_t {
       if constexpr (KIND == kKindLcg) return (la * c + lc) & mask32;
       else if constexpr (kFast) return philox_keys_fwd<D, 24>(c, kr, p.L, p.R, p.LM, p.RM, 24);
-      else return philox_keys_fwd<D, 0>(c, s_keys, p.L, p.R, p.LM, p.RM, p.rounds);
+      else return philox_keys_fwd<D, 0>(c, keys, p.L, p.R, p.LM, p.RM, p.rounds);
     };
     if (pow2) {
+#pragma unroll 4
       for (uint32_t c = tid; c < n; c += kThreads) st_out<T>(row_out + c, s_row[f(c)]);
     } else {
       uint32_t base = 0;
-      int buf = 0;
+      int cb = 0;
       for (uint32_t c0 = 0; c0 < n; c0 += kThreads) {
         const uint32_t c = c0 + tid;
         const uint32_t y = f(c);
-        const bool keep = y < m;  // c < n always (n is a multiple of 256 or the loop is single)
-        const uint32_t bm = __ballot_sync(0xFFFFFFFFu, keep && c < n);
-        if (lane == 0) s_wcnt[buf][warp] = __popc(bm);
+        const bool keep = (c < n) && (y < m);
+        const uint32_t bm = __ballot_sync(0xFFFFFFFFu, keep);
+        if (lane == 0) s_wcnt[cb][warp] = __popc(bm);
         __syncthreads();
         uint32_t before = 0, total = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-          const uint32_t x = s_wcnt[buf][w];
+          const uint32_t x = s_wcnt[cb][w];
           before += (w < warp) ? x : 0;
           total += x;
         }
-        if (keep && c < n) st_out<T>(row_out + base + before + __popc(bm & lanemask_lt()), s_row[y]);
+        if (keep) st_out<T>(row_out + base + before + __popc(bm & lanemask_lt()), s_row[y]);
         base += total;
-        buf ^= 1;  // double-buffered counts: one barrier per chunk
+        cb ^= 1;  // double-buffered counts: one barrier per chunk
       }
     }
-    __syncthreads();  // s_row / s_keys reuse by the next shuffle
+    __syncthreads();  // buffer `buf` and its keys are refilled two iterations later
   }
 }
 

@@ -29,7 +29,7 @@ cudaError_t launch_shuffle(int elem_code, const ShuffleLaunch& a, cudaStream_t s
 bool batched_supported(int elem_code, uint32_t m, int bits, int rounds) {
   if (elem_code != 1 && elem_code != 2 && elem_code != 4 && elem_code != 8 && elem_code != 16) return false;
   if (bits > 16 || rounds > kBatchedMaxRounds) return false;
-  return static_cast<uint64_t>(m) * elem_code <= 160u * 1024u;
+  return static_cast<uint64_t>(m) * elem_code <= 96u * 1024u;  // two row buffers in shared memory
 }
 
 cudaError_t launch_batched(int elem_code, const BatchedLaunch& a, cudaStream_t s) {
