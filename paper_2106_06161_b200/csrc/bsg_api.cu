@@ -246,7 +246,7 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
   L.compact = !pow2 || g_force_compact;
   L.count_out = count_dev;
   if (L.compact) {
-    const uint64_t tile = bsg::kCompactTile;
+    const uint64_t tile = bsg::kCompactTileMin;  // sizes the status words for the smallest tile
     BSG_TRY(lookback_prepare(c, (c1 - c0 + tile - 1) / tile, s, L.lb));
   }
   if (c1 > c0) BSG_CUDA(bsg::launch_shuffle(elem_code, L, s));

@@ -21,14 +21,18 @@ cudaError_t run_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
     k_pow2<KIND, CT, T, SH, kPow2Items><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a.src, a.out, a.c0, a.c1,
                                                                                          a.p);
   } else {
-    constexpr uint64_t kTile = kThreads * kCompactItems;
+    // 16-byte payloads keep 8 items so the static shared staging stays under 48 KiB.
+    constexpr int kItems = (sizeof(T) >= 16) ? 8 : kCompactItems;
+    constexpr uint64_t kTile = kThreads * kItems;
     const uint64_t grid = (len + kTile - 1) / kTile;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     if constexpr (sizeof(T) >= 4 || std::is_same<T, IdxTag>::value) {
-      k_compact_smem<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+      k_compact_smem<KIND, CT, T, SH, kItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
           a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
     } else {
-      k_compact<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+      constexpr uint64_t kTileR = kThreads * kCompactItems;
+      const uint64_t gridr = (len + kTileR - 1) / kTileR;
+      k_compact<KIND, CT, T, SH, kCompactItems><<<static_cast<unsigned>(gridr), kThreads, 0, s>>>(
           a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
     }
   }

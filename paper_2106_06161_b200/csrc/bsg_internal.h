@@ -21,6 +21,7 @@ constexpr int kThreads = 256;
 constexpr int kPow2Items = BSG_POW2_ITEMS;        // counters per thread, pow2 kernel
 constexpr int kCompactItems = BSG_COMPACT_ITEMS;  // counters per thread, compacting (look-back) kernel
 constexpr uint64_t kCompactTile = static_cast<uint64_t>(kThreads) * kCompactItems;
+constexpr uint64_t kCompactTileMin = static_cast<uint64_t>(kThreads) * 8;  // smallest tile of any payload type
 constexpr int kBatchedMaxRounds = 64;
 
 struct IdxTag {};  // "payload" of shuffle_indices: the image itself, written as u64

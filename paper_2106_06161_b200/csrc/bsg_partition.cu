@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
   uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);
-  __shared__ uint32_t hist[kMaxB1], start[kMaxB1], gbase[kMaxB1], wt[32];
+  __shared__ uint32_t hist[kMaxB1], start[kMaxB1], wt[32];
+  __shared__ unsigned long long delta[kMaxB1];
   const int tid = threadIdx.x;
   for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
   __syncthreads();
@@ -115,7 +116,10 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
   }
   __syncthreads();
   scan_bins(hist, start, nb, wt);
-  for (int i = tid; i < nb; i += kP1Threads) gbase[i] = atomicAdd(cur1 + i, hist[i]);
+  for (int i = tid; i < nb; i += kP1Threads) {
+    // one table lookup per element in the write-back: global position = delta[b] + slot
+    delta[i] = static_cast<unsigned long long>(i) * w1 + atomicAdd(cur1 + i, hist[i]) - start[i];
+  }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
@@ -126,8 +130,8 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
   __syncthreads();
 #pragma unroll 4
   for (int s = tid; s < kP1Tile; s += kP1Threads) {
-    const uint32_t d = sd[s], b = d >> bshift;
-    const uint64_t pos = b * w1 + gbase[b] + (s - start[b]);
+    const uint32_t d = sd[s];
+    const uint64_t pos = delta[d >> bshift] + s;
     __stcs(tv + pos, sv[s]);
     __stcs(td + pos, d);
   }
@@ -141,9 +145,9 @@ __global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, 
                                                          uint64_t w1) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
-  uint16_t* sd = reinterpret_cast<uint16_t*>(sv + kP2Tile);
-  uint8_t* sb = reinterpret_cast<uint8_t*>(sd + kP2Tile);
-  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], gbase[kMaxB2], wt[32];
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
+  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], wt[32];
+  __shared__ unsigned long long delta[kMaxB2];
   const int tid = threadIdx.x;
   if (tid < nb2) hist[tid] = 0;
   __syncthreads();
@@ -162,24 +166,23 @@ __global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, 
   __syncthreads();
   scan_bins(hist, start, nb2, wt);
   uint32_t* cur = cur2 + coarse * nb2;
-  if (tid < nb2) gbase[tid] = atomicAdd(cur + tid, hist[tid]);
+  const uint64_t win0 = coarse * w1;  // first element of this coarse bucket's output range
+  if (tid < nb2)
+    delta[tid] = win0 + (static_cast<unsigned long long>(tid) << w2) + atomicAdd(cur + tid, hist[tid]) - start[tid];
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kP2Items; ++i) {
-    const uint32_t f = (d[i] >> w2) & fmask;
-    const uint32_t s = start[f] + rk[i];
+    const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
     sv[s] = v[i];
-    sd[s] = static_cast<uint16_t>(d[i] & wmask);
-    sb[s] = static_cast<uint8_t>(f);
+    sd[s] = d[i];
   }
   __syncthreads();
-  const uint64_t win0 = coarse * w1;  // first element of this coarse bucket's output range
 #pragma unroll 4
   for (int s = tid; s < kP2Tile; s += kP2Threads) {
-    const uint32_t f = sb[s];
-    const uint64_t pos = win0 + (static_cast<uint64_t>(f) << w2) + gbase[f] + (s - start[f]);
+    const uint32_t dd = sd[s];
+    const uint64_t pos = delta[(dd >> w2) & fmask] + s;
     ov[pos] = sv[s];
-    od[pos] = sd[s];
+    od[pos] = static_cast<uint16_t>(dd & wmask);
   }
 }
 
@@ -222,7 +225,10 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   const int b = a.p.bits;
   const int w2 = window_log2<T>();
   const int total = b - w2;
-  const int s1 = (total + 1) / 2, s2 = total - s1;
+#ifndef BSG_PART_S1_BIAS
+#define BSG_PART_S1_BIAS 0
+#endif
+  const int s1 = (total + 1) / 2 + BSG_PART_S1_BIAS, s2 = total - s1;
   const uint64_t n = 1ULL << b, w1 = 1ULL << (b - s1);
   const int nb1 = 1 << s1, nb2 = 1 << s2;
   uint32_t* cur1 = a.cursors;
@@ -230,7 +236,7 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(a.cursors, 0, (static_cast<size_t>(nb1) + static_cast<size_t>(nb1) * nb2) * 4, s);
   if (e != cudaSuccess) return e;
   const size_t sm1 = kP1Tile * (sizeof(T) + 4);
-  const size_t sm2 = kP2Tile * (sizeof(T) + 3);
+  const size_t sm2 = kP2Tile * (sizeof(T) + 4);
   const size_t sm3 = (size_t{1} << w2) * sizeof(T);
   cudaFuncSetAttribute(k_part1<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
   cudaFuncSetAttribute(k_part2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
@@ -425,7 +431,7 @@ bool partition_eligible(int elem_code, int bits) {
     default: return false;
   }
   const int total = bits - w2;
-  const int s1 = (total + 1) / 2, s2 = total - s1;
+  const int s1 = (total + 1) / 2 + BSG_PART_S1_BIAS, s2 = total - s1;
   // fan-outs within the shared-memory histograms; tiles must not straddle buckets; 32-bit destinations
   return bits <= 32 && s1 >= 1 && s2 >= 1 && (1 << s1) <= kMaxB1 && (1 << s2) <= kMaxB2 &&
          (bits - s1) >= 12 && bits >= 14;
