@@ -1,0 +1,26 @@
+"""compute-sanitizer over every kernel family at small sizes: out-of-bounds
+(memcheck) and shared-memory races (racecheck) in the look-back, partition,
+batched and routing kernels."""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_clean(tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_run.py")], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "sanitize-run OK" in r.stdout

@@ -1,0 +1,55 @@
+"""Small shuffles through every kernel family, for compute-sanitizer (memcheck/racecheck/synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+import numpy as np, torch
+import oracle as O
+import paper_2106_06161_b200 as bsg
+from paper_2106_06161_b200 import distributed as D
+
+ok = True
+def check(name, got, exp):
+    global ok
+    if not np.array_equal(got, exp):
+        ok = False
+        print("MISMATCH", name)
+
+for m, v in ((5000, 1), ((1 << 14) + 3, 0), (1 << 12, 1)):
+    cfg = bsg.ShuffleConfig(seed=m, variant=bsg.BijectionVariant(v))
+    vals = torch.arange(m, dtype=torch.int64, device="cuda")
+    check(f"values {m}", bsg.shuffle_values(vals, cfg).cpu().numpy().view(np.uint64), O.shuffle_indices(m, m, v, 24))
+    check(f"indices {m}", bsg.shuffle_indices(m, cfg, device="cuda").cpu().numpy().view(np.uint64),
+          O.shuffle_indices(m, m, v, 24))
+bsg.set_force_compact(True)
+check("forced compact", bsg.shuffle_indices(1 << 13, bsg.ShuffleConfig(seed=3), device="cuda").cpu().numpy().view(np.uint64),
+      O.shuffle_indices(1 << 13, 3))
+bsg.set_force_compact(False)
+bsg.set_path(2)
+vals = torch.arange(1 << 16, dtype=torch.int64, device="cuda")
+check("partitioned", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=9)).cpu().numpy().view(np.uint64),
+      O.shuffle_indices(1 << 16, 9))
+bsg.set_path(0)
+rows = torch.arange(1024, dtype=torch.int32, device="cuda").repeat(16, 1)
+out = bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=1000)).cpu().numpy()
+for b in range(16):
+    check(f"batched {b}", out[b].astype(np.uint64), O.shuffle_indices(1024, 1000 + b))
+rows = torch.arange(1000, dtype=torch.int32, device="cuda").repeat(8, 1)
+out = bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=5)).cpu().numpy()
+for b in range(8):
+    check(f"batched1000 {b}", out[b].astype(np.uint64), O.shuffle_indices(1000, 5 + b))
+m, W = 1 << 16, 4
+S = m // W
+full = torch.arange(m, dtype=torch.int64, device="cuda")
+cfg = bsg.ShuffleConfig(seed=11)
+routed = [D._gpu_route(full[r * S:(r + 1) * S].contiguous(), m, cfg, r, W) for r in range(W)]
+parts = []
+for dst in range(W):
+    vs = [routed[s][0][sum(routed[s][2][:dst]):sum(routed[s][2][:dst + 1])] for s in range(W)]
+    ds = [routed[s][1][sum(routed[s][2][:dst]):sum(routed[s][2][:dst + 1])] for s in range(W)]
+    parts.append(D._gpu_scatter(torch.cat(vs), torch.cat(ds), S))
+check("sharded", torch.cat(parts).cpu().numpy().view(np.uint64), O.shuffle_indices(m, 11))
+idx = torch.randint(0, 1 << 12, (5000,), device="cuda")
+src = torch.arange(1 << 12, dtype=torch.int64, device="cuda")
+check("gather", bsg.gather(src, idx).cpu().numpy(), src.cpu().numpy()[idx.cpu().numpy()])
+torch.cuda.synchronize()
+print("sanitize-run", "OK" if ok else "FAILED")
