@@ -496,8 +496,12 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
     const uint32_t* keys = s_keys[buf];
     T* row_out = out + b * m;
     const uint64_t sb = seed + b;
-    uint32_t kr[kFast ? 24 : 1];
-    if constexpr (kFast) {
+#ifndef BSG_BATCHED_SMEM_KEYS
+#define BSG_BATCHED_SMEM_KEYS 0
+#endif
+    constexpr bool kRegKeys = kFast && !BSG_BATCHED_SMEM_KEYS;
+    uint32_t kr[kRegKeys ? 24 : 1];
+    if constexpr (kRegKeys) {
 #pragma unroll
       for (int i = 0; i < 24; ++i) kr[i] = keys[i];
     }
@@ -506,7 +510,8 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
     const uint32_t lc = static_cast<uint32_t>(mix64(sb + 1)) & mask32;
     auto f = [&](uint32_t c) -> uint32_t {
       if constexpr (KIND == kKindLcg) return (la * c + lc) & mask32;
-      else if constexpr (kFast) return philox_keys_fwd<D, 24>(c, kr, p.L, p.R, p.LM, p.RM, 24);
+      else if constexpr (kRegKeys) return philox_keys_fwd<D, 24>(c, kr, p.L, p.R, p.LM, p.RM, 24);
+      else if constexpr (kFast) return philox_keys_fwd<D, 24>(c, keys, p.L, p.R, p.LM, p.RM, 24);
       else return philox_keys_fwd<D, 0>(c, keys, p.L, p.R, p.LM, p.RM, p.rounds);
     };
     if (pow2) {
