@@ -104,9 +104,16 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
   for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
   __syncthreads();
   const uint32_t base = blockIdx.x * kP1Tile + tid;
-  T v[kP1Items];
+#ifndef BSG_P1_LATE_LOAD
+#define BSG_P1_LATE_LOAD 1
+#endif
+  // Default: the input tile is loaded first (its latency hides under the cipher).  LATE_LOAD keeps the
+  // values out of registers during the cipher (more resident CTAs) and loads them after the scan.
+  T v[BSG_P1_LATE_LOAD ? 1 : kP1Items];
+  if constexpr (!BSG_P1_LATE_LOAD) {
 #pragma unroll
-  for (int i = 0; i < kP1Items; ++i) v[i] = __ldcs(in + base + i * kP1Threads);
+    for (int i = 0; i < kP1Items; ++i) v[i] = __ldcs(in + base + i * kP1Threads);
+  }
   uint32_t dst[kP1Items], rk[kP1Items];
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
@@ -124,7 +131,8 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
     const uint32_t s = start[dst[i] >> bshift] + rk[i];
-    sv[s] = v[i];
+    if constexpr (BSG_P1_LATE_LOAD) sv[s] = __ldcs(in + base + i * kP1Threads);
+    else sv[s] = v[i];
     sd[s] = dst[i];
   }
   __syncthreads();
