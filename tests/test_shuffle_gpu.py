@@ -452,3 +452,23 @@ def test_scatter_permutation_paths(bsg, cuda):
             assert cuda.equal(out, ref), (n, path)
         finally:
             bsg.set_path(old)
+
+
+def test_partitioned_16_byte_payload(bsg, cuda):
+    """16-byte records through the partitioned path and the single pass, via the C ABI."""
+    from paper_2106_06161_b200 import _lib
+    m = 1 << 20
+    rec = cuda.arange(2 * m, dtype=cuda.int64, device="cuda").view(m, 2)
+    exp = O.shuffle_indices(m, 44)
+    for path in (1, 2):
+        old = bsg.set_path(path)
+        try:
+            out = cuda.empty_like(rec)
+            _lib.check(_lib.lib.bsg_shuffle_values(rec.data_ptr(), out.data_ptr(), m, 16,
+                                                   ctypes.byref(cfg_of(bsg, seed=44)._c()), None), "u128")
+            cuda.cuda.synchronize()
+            got = out.cpu().numpy()
+            assert np.array_equal(got[:, 0].astype(np.uint64), 2 * exp), path
+            assert np.array_equal(got[:, 1].astype(np.uint64), 2 * exp + 1), path
+        finally:
+            bsg.set_path(old)
