@@ -23,6 +23,8 @@
 // irrelevant -- the output is bit-identical to the single-pass kernel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "bsg_kernels.cuh"
 #include "bsg_partition.h"
 
@@ -150,7 +152,7 @@ template <typename T>
 __global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                          T* __restrict__ ov, uint16_t* __restrict__ od,
                                                          uint32_t* __restrict__ cur2, int w2, int nb2,
-                                                         uint64_t w1) {
+                                                         uint64_t w1, uint64_t tile_base) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
   uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, 
   const int tid = threadIdx.x;
   if (tid < nb2) hist[tid] = 0;
   __syncthreads();
-  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kP2Tile;
+  const uint64_t t0 = (tile_base + blockIdx.x) * kP2Tile;
   const uint64_t coarse = t0 / w1;
   const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
   T v[kP2Items];
@@ -196,13 +198,13 @@ __global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, 
 
 // P3: place each fine window through shared memory, in place in `out`.
 template <typename T>
-__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, const uint16_t* __restrict__ od,
-                                                      int w2) {
+__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2,
+                                                      uint64_t win_base, int discard) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* win = reinterpret_cast<T*>(smem);
   const uint32_t W = 1u << w2;
-  T* o = out + (static_cast<uint64_t>(blockIdx.x) << w2);
-  const uint16_t* dd = od + (static_cast<uint64_t>(blockIdx.x) << w2);
+  T* o = out + ((win_base + blockIdx.x) << w2);
+  uint16_t* dd = od + ((win_base + blockIdx.x) << w2);
   constexpr int kU = 8;
   for (uint32_t i0 = threadIdx.x; i0 < W; i0 += kP3Threads * kU) {
     T v[kU];
@@ -220,6 +222,11 @@ __global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, const
       if (i0 + u * kP3Threads < W) win[d[u]] = v[u];
   }
   __syncthreads();
+  if (discard) {
+    // The window's u16 destinations are dead: drop their (L2-resident, dirty) lines without write-back.
+    for (uint32_t l = threadIdx.x; l < (W * 2) / 128; l += kP3Threads)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(dd) + l * 128) : "memory");
+  }
   for (uint32_t i = threadIdx.x; i < W; i += kP3Threads) __stcs(o + i, win[i]);
 }
 
@@ -252,10 +259,25 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   T* tv = static_cast<T*>(a.tmp_values);
   k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
       static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in);
-  k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
-                                                                          a.tmp_dlow, cur2, w2, nb2, w1);
-  k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2);
-  note_launch(3);
+#ifndef BSG_PART_GROUP_MB
+#define BSG_PART_GROUP_MB 0
+#endif
+  // Grouped mode: P2 and P3 alternate over groups of coarse buckets sized to stay resident in L2, so P3
+  // reads P2's output from L2 and its dead destination lines are discarded instead of written back.
+  const uint64_t bucket_bytes = w1 * (sizeof(T) + 2);
+  const uint64_t group = BSG_PART_GROUP_MB > 0
+                             ? std::max<uint64_t>(1, (static_cast<uint64_t>(BSG_PART_GROUP_MB) << 20) / bucket_bytes)
+                             : static_cast<uint64_t>(nb1);
+  uint64_t launched = 1;
+  for (uint64_t c0 = 0; c0 < static_cast<uint64_t>(nb1); c0 += group) {
+    const uint64_t cn = std::min<uint64_t>(group, nb1 - c0);
+    k_part2<T><<<static_cast<unsigned>(cn * w1 / kP2Tile), kP2Threads, sm2, s>>>(
+        tv, a.tmp_dest, static_cast<T*>(a.out), a.tmp_dlow, cur2, w2, nb2, w1, c0 * w1 / kP2Tile);
+    k_place<T><<<static_cast<unsigned>(cn * w1 >> w2), kP3Threads, sm3, s>>>(
+        static_cast<T*>(a.out), a.tmp_dlow, w2, c0 * w1 >> w2, BSG_PART_GROUP_MB > 0 ? 1 : 0);
+    launched += 2;
+  }
+  note_launch(launched);
   return cudaGetLastError();
 }
 
