@@ -246,7 +246,13 @@ def ours_arm(args, rank, world, local):
                                                       None, out.data_ptr(), eb, cnt_dev.data_ptr(),
                                                       stream.cuda_stream), "shuffle_range")
                 dist.all_gather_into_tensor(counts, cnt_dev)  # the 8-byte count exchange (NCCL)
-        dominant = ("bsg::k_part1+k_part2+k_place" if (m_total & (m_total - 1)) == 0 and m_total * eb >= (256 << 20) else "bsg::k_pow2") if (m_total & (m_total - 1)) == 0 else "bsg::k_compact_smem"
+        pow2 = (m_total & (m_total - 1)) == 0
+        if not pow2:
+            dominant = "bsg::k_compact_smem"
+        elif world == 1 and m_total * eb >= (256 << 20):
+            dominant = "bsg::k_part1+k_part2+k_place"  # partitioned path (whole domain, >= 256 MiB)
+        else:
+            dominant = "bsg::k_pow2"  # counter-range shards take the single fused pass
 
     def barrier():
         torch.cuda.synchronize(dev)

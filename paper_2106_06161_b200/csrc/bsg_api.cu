@@ -227,11 +227,7 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
       P.cursors = reinterpret_cast<uint32_t*>(w + n * elem_code + n * 6);
       P.p = p;
       BSG_CUDA(bsg::launch_partition(elem_code, P, s));
-      if (count_dev) {
-        const unsigned long long cnt = n;
-        BSG_CUDA(cudaMemcpyAsync(count_dev, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
-        BSG_CUDA(cudaStreamSynchronize(s));
-      }
+      if (count_dev) BSG_CUDA(bsg::launch_store_u64(count_dev, n, s));
       return ws_end(c, s);
     }
     cudaGetLastError();  // workspace did not fit: the single-pass kernel needs none
@@ -250,11 +246,7 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
     BSG_TRY(lookback_prepare(c, (c1 - c0 + tile - 1) / tile, s, L.lb));
   }
   if (c1 > c0) BSG_CUDA(bsg::launch_shuffle(elem_code, L, s));
-  if (count_dev && (!L.compact || c1 == c0)) {
-    const unsigned long long n = c1 - c0;
-    BSG_CUDA(cudaMemcpyAsync(count_dev, &n, sizeof(n), cudaMemcpyHostToDevice, s));
-    BSG_CUDA(cudaStreamSynchronize(s));
-  }
+  if (count_dev && (!L.compact || c1 == c0)) BSG_CUDA(bsg::launch_store_u64(count_dev, c1 - c0, s));
   return ws_end(c, s);
 }
 

@@ -106,6 +106,8 @@ cudaError_t sort_shuffle_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint
 cudaError_t launch_count(uint64_t m, uint64_t c0, uint64_t c1, const BijParams& p, unsigned long long* count,
                          cudaStream_t s);
 
+cudaError_t launch_store_u64(unsigned long long* p, uint64_t v, cudaStream_t s);
+
 // Count of our kernel launches since load (bench.py's gpu_launches).
 void note_launch(uint64_t k = 1);
 uint64_t launches();

@@ -129,6 +129,15 @@ cudaError_t launch_map(const uint64_t* x, uint64_t* y, uint64_t n, uint64_t star
   return cudaErrorInvalidValue;
 }
 
+__global__ void k_store_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+// Writes a known survivor count on the stream (closed form for power-of-two ranges) without a host sync.
+cudaError_t launch_store_u64(unsigned long long* p, uint64_t v, cudaStream_t s) {
+  k_store_u64<<<1, 1, 0, s>>>(p, v);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // Count-only pass: survivors among counters [c0, c1) (multi-GPU pre-count).
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) k_count(uint64_t m, uint64_t c0, uint64_t c1, BijParams p,
