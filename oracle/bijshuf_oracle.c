@@ -24,6 +24,7 @@
  */
 #include <stddef.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define ORC_OK 0
@@ -170,15 +171,17 @@ int orc_shuffle_indices(uint64_t m, uint64_t seed, int variant, int rounds, uint
     out[1] = bit ^ 1;
     return ORC_OK;
   }
-  static orc_bij b; /* large key table; the oracle is single-threaded */
-  int rc = orc_bij_init(&b, m, seed, variant, rounds);
-  if (rc) return rc;
-  const uint64_t n = 1ULL << b.bits;
+  orc_bij* b = (orc_bij*)malloc(sizeof(orc_bij)); /* key table per call: reentrant */
+  if (!b) return ORC_EINVAL;
+  int rc = orc_bij_init(b, m, seed, variant, rounds);
+  if (rc) { free(b); return rc; }
+  const uint64_t n = 1ULL << b->bits;
   uint64_t k = 0;
   for (uint64_t i = 0; i < n; ++i) {
-    const uint64_t y = orc_bij_apply(&b, i);
+    const uint64_t y = orc_bij_apply(b, i);
     if (y < m) out[k++] = y;
   }
+  free(b);
   return ORC_OK;
 }
 
@@ -191,20 +194,22 @@ int orc_shuffle_indices_range(uint64_t m, uint64_t seed, int variant, int rounds
                               uint64_t* out, uint64_t* count) {
   *count = 0;
   if (m <= 2) return ORC_EINVAL;
-  static orc_bij b;
-  int rc = orc_bij_init(&b, m, seed, variant, rounds);
-  if (rc) return rc;
-  const uint64_t n = 1ULL << b.bits;
-  if (c1 > n || c0 > c1) return ORC_ERANGE;
+  orc_bij* b = (orc_bij*)malloc(sizeof(orc_bij));
+  if (!b) return ORC_EINVAL;
+  int rc = orc_bij_init(b, m, seed, variant, rounds);
+  if (rc) { free(b); return rc; }
+  const uint64_t n = 1ULL << b->bits;
+  if (c1 > n || c0 > c1) { free(b); return ORC_ERANGE; }
   uint64_t k = 0;
   for (uint64_t i = c0; i < c1; ++i) {
-    const uint64_t y = orc_bij_apply(&b, i);
+    const uint64_t y = orc_bij_apply(b, i);
     if (y < m) {
       if (out) out[k] = y;
       ++k;
     }
   }
   *count = k;
+  free(b);
   return ORC_OK;
 }
 
@@ -222,15 +227,17 @@ int orc_shuffle_values(const void* values, void* out, uint64_t m, size_t elem_by
     memcpy(d + elem_bytes, s + (bit ^ 1) * elem_bytes, elem_bytes);
     return ORC_OK;
   }
-  static orc_bij b;
-  int rc = orc_bij_init(&b, m, seed, variant, rounds);
-  if (rc) return rc;
-  const uint64_t n = 1ULL << b.bits;
+  orc_bij* b = (orc_bij*)malloc(sizeof(orc_bij));
+  if (!b) return ORC_EINVAL;
+  int rc = orc_bij_init(b, m, seed, variant, rounds);
+  if (rc) { free(b); return rc; }
+  const uint64_t n = 1ULL << b->bits;
   uint64_t k = 0;
   for (uint64_t i = 0; i < n; ++i) {
-    const uint64_t y = orc_bij_apply(&b, i);
+    const uint64_t y = orc_bij_apply(b, i);
     if (y < m) memcpy(d + (k++) * elem_bytes, s + y * elem_bytes, elem_bytes);
   }
+  free(b);
   return ORC_OK;
 }
 

@@ -472,3 +472,43 @@ def test_partitioned_16_byte_payload(bsg, cuda):
             assert np.array_equal(got[:, 1].astype(np.uint64), 2 * exp + 1), path
         finally:
             bsg.set_path(old)
+
+
+def test_concurrent_callers_on_separate_streams(bsg, cuda):
+    """Host threads on their own CUDA streams share one device context (look-back workspace,
+    key buffer, partition workspace): results must stay exact."""
+    import threading
+    sizes = [(1 << 20) + 7, 1 << 21, 5000, (1 << 18) + 1, 1 << 16, 123457]
+    errors = []
+
+    def worker(tid):
+        try:
+            s = cuda.cuda.Stream()
+            with cuda.cuda.stream(s):
+                for it in range(4):
+                    m = sizes[(tid + it) % len(sizes)]
+                    seed = tid * 100 + it
+                    vals = cuda.arange(m, dtype=cuda.int64, device="cuda")
+                    out = bsg.shuffle_values(vals, cfg_of(bsg, seed=seed, rounds=24 if it % 2 else 12))
+                    s.synchronize()
+                    exp = O.shuffle_indices(m, seed, PHILOX, 24 if it % 2 else 12)
+                    if not np.array_equal(out.cpu().numpy().view(np.uint64), exp):
+                        errors.append((tid, it, m))
+        except Exception as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
+def test_pipeline_with_pageable_buffers(bsg, cuda):
+    m = 70001
+    a = np.arange(m, dtype=np.uint64)
+    b = np.empty_like(a)
+    with bsg.Pipeline(m, 8) as pipe:
+        pipe.wait(pipe.submit(a, b, cfg_of(bsg, seed=31)))
+    assert np.array_equal(b, O.shuffle_indices(m, 31))
