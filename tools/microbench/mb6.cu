@@ -29,6 +29,36 @@ __device__ __forceinline__ uint32_t inv(uint32_t y, const P& p) {
   return (t0 << p.R) | (t1 & p.RM);
 }
 
+// FP64-assisted inverse round (d=1): one DFMA gives both words of s0*M0lo (exact, < 2^52).
+__device__ __forceinline__ uint32_t inv_fp(uint32_t y, const P& p) {
+  const double M = (double)M0LO, C = 4503599627370496.0 - 4503599627370496.0 * (double)M0LO;
+  uint32_t t0 = y >> p.R, t1 = y & p.RM;
+#pragma unroll
+  for (int i = 23; i >= 0; --i) {
+    const uint32_t s0 = ((t1 >> 1) * INV) & p.LM;
+    const double r = fma(__hiloint2double(0x43300000, (int)s0), M, C);
+    const uint32_t hi = (uint32_t)__double2hiint(r) + s0 * M0HI;
+    const uint32_t x = (hi ^ p.k[i] ^ t0) & p.LM;
+    t0 = s0;
+    t1 = t1 * p.shl + x;
+  }
+  return (t0 << p.R) | (t1 & p.RM);
+}
+
+// integer inverse with the OR folded into the spare-bit IMAD
+__device__ __forceinline__ uint32_t inv_addend(uint32_t y, const P& p) {
+  uint32_t t0 = y >> p.R, t1 = y & p.RM;
+#pragma unroll
+  for (int i = 23; i >= 0; --i) {
+    const uint32_t s0 = ((t1 >> 1) * INV) & p.LM;
+    const uint32_t hi = __umulhi(s0, M0LO) + s0 * M0HI;
+    const uint32_t x = (hi ^ p.k[i] ^ t0) & p.LM;
+    t0 = s0;
+    t1 = t1 * p.shl + x;
+  }
+  return (t0 << p.R) | (t1 & p.RM);
+}
+
 template <int V>
 __device__ __forceinline__ uint32_t fwd(uint32_t x, const P& p) {
   uint32_t s0 = x >> p.R, s1 = x & p.RM;
@@ -61,9 +91,20 @@ __global__ void __launch_bounds__(256) k(uint32_t n, P p, uint32_t* sink) {
   uint32_t acc = 0;
   for (uint32_t b = blockIdx.x * 1024 + threadIdx.x; b < n; b += gridDim.x * 1024) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc += (V >= 8) ? fwd<V>(b + j * 256, p) : inv<V>(b + j * 256, p);
+    for (int j = 0; j < 4; ++j) {
+      if (V == 20) acc += inv_fp(b + j * 256, p);
+      else if (V == 21) acc += inv_addend(b + j * 256, p);
+      else acc += (V >= 8) ? fwd<V>(b + j * 256, p) : inv<V>(b + j * 256, p);
+    }
   }
   if (acc == 0x1234567u) sink[0] = acc;
+}
+
+__global__ void k_chk(P p, unsigned long long* bad) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < (1u << 29); x += gridDim.x * blockDim.x) {
+    const uint32_t a = inv<2>(x, p);
+    if (inv_fp(x, p) != a || inv_addend(x, p) != a) atomicAdd(bad, 1ull);
+  }
 }
 
 int main() {
@@ -79,11 +120,22 @@ int main() {
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); ms /= 5;
     printf("%-40s 2^29 inverse ciphers %7.3f ms  %7.1f G/s\n", name, ms, n / ms / 1e6);
   };
+  {
+    unsigned long long* bad; CK(cudaMalloc(&bad, 8)); CK(cudaMemset(bad, 0, 8));
+    k_chk<<<148 * 8, 256>>>(p, bad); unsigned long long hb; CK(cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost));
+    printf("variant mismatches over 2^29 inputs: %llu\n", hb);
+  }
   run(k<0>, "SHF >>1, SHF <<L");
   run(k<1>, "IMAD.HI >>1, SHF <<L");
   run(k<2>, "SHF >>1, IMAD <<L");
   run(k<3>, "IMAD.HI >>1, IMAD <<L");
   run(k<6>, "inv: SHF >>1, IMAD <<L, WIDE hi");
+  run(k<20>, "inv: DFMA hi, IMAD spare+x");
+  run(k<21>, "inv: IMAD.HI hi, IMAD spare+x");
+  {  // equality check of the variants on 2^22 inputs
+    uint32_t* d; CK(cudaMalloc(&d, 4 * 3));
+    printf("check: see k_chk\n");
+  }
   run(k<8>, "fwd d1: HI, lo=IMAD|t (current)");
   run(k<9>, "fwd d1: WIDE, lo=IMAD(wlo,2,t)");
   run(k<10>, "fwd d1: WIDE, lo=(wlo<<1)|t");
