@@ -89,6 +89,7 @@ __device__ __forceinline__ void scan_bins(const uint32_t* hist, uint32_t* start,
     if (k < per && idx < nb) start[idx] = run;
     run += loc[k];
   }
+  __syncthreads();  // start[] is read by other threads right after (two bins per thread when nb > blockDim)
 }
 
 // P1: stream the input, route by coarse destination bucket.
@@ -196,6 +197,81 @@ __global__ void __launch_bounds__(kP2Threads) k_part2(const T* __restrict__ tv, 
   }
 }
 
+// Persistent P2: each CTA loops over tiles; the next tile's values and
+// destinations stream into shared memory with cp.async while the current tile
+// is ranked, scattered and written, so the load latency leaves the critical path.
+template <typename T>
+__global__ void __launch_bounds__(kP2Threads) k_part2p(const T* __restrict__ tv, const uint32_t* __restrict__ td,
+                                                          T* __restrict__ ov, uint16_t* __restrict__ od,
+                                                          uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
+                                                          uint64_t tile_base, uint64_t ntiles) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sv = reinterpret_cast<T*>(smem);
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
+  T* iv = reinterpret_cast<T*>(sd + kP2Tile);
+  uint32_t* id = reinterpret_cast<uint32_t*>(iv + kP2Tile);
+  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], wt[32];
+  __shared__ unsigned long long delta[kMaxB2];
+  const int tid = threadIdx.x;
+  const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
+  auto prefetch = [&](uint64_t t) {
+    const char* gv = reinterpret_cast<const char*>(tv + (tile_base + t) * kP2Tile);
+    const char* gd = reinterpret_cast<const char*>(td + (tile_base + t) * kP2Tile);
+    for (uint32_t o = tid * 16; o < kP2Tile * sizeof(T); o += kP2Threads * 16) {
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(reinterpret_cast<char*>(iv) + o));
+      asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst), "l"(gv + o) : "memory");
+    }
+    for (uint32_t o = tid * 16; o < kP2Tile * 4; o += kP2Threads * 16) {
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(reinterpret_cast<char*>(id) + o));
+      asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst), "l"(gd + o) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  uint64_t t = blockIdx.x;
+  if (t < ntiles) prefetch(t);
+  for (; t < ntiles; t += gridDim.x) {
+    if (tid < nb2) hist[tid] = 0;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    T v[kP2Items];
+    uint32_t d[kP2Items], rk[kP2Items];
+#pragma unroll
+    for (int i = 0; i < kP2Items; ++i) {
+      v[i] = iv[tid + i * kP2Threads];
+      d[i] = id[tid + i * kP2Threads];
+    }
+    __syncthreads();  // input buffer free: stream the next tile in behind this one
+    if (t + gridDim.x < ntiles) prefetch(t + gridDim.x);
+#pragma unroll
+    for (int i = 0; i < kP2Items; ++i) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
+    __syncthreads();
+    scan_bins(hist, start, nb2, wt);
+    const uint64_t t0 = (tile_base + t) * kP2Tile;
+    const uint64_t coarse = t0 / w1;
+    uint32_t* cur = cur2 + coarse * nb2;
+    const uint64_t win0 = coarse * w1;
+    if (tid < nb2)
+      delta[tid] =
+          win0 + (static_cast<unsigned long long>(tid) << w2) + atomicAdd(cur + tid, hist[tid]) - start[tid];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kP2Items; ++i) {
+      const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
+      sv[s] = v[i];
+      sd[s] = d[i];
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int s = tid; s < kP2Tile; s += kP2Threads) {
+      const uint32_t dd = sd[s];
+      const uint64_t pos = delta[(dd >> w2) & fmask] + s;
+      ov[pos] = sv[s];
+      od[pos] = static_cast<uint16_t>(dd & wmask);
+    }
+    __syncthreads();  // staging reuse by the next tile
+  }
+}
+
 // P3: place each fine window through shared memory, in place in `out`.
 template <typename T>
 __global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2,
@@ -271,8 +347,25 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   uint64_t launched = 1;
   for (uint64_t c0 = 0; c0 < static_cast<uint64_t>(nb1); c0 += group) {
     const uint64_t cn = std::min<uint64_t>(group, nb1 - c0);
-    k_part2<T><<<static_cast<unsigned>(cn * w1 / kP2Tile), kP2Threads, sm2, s>>>(
-        tv, a.tmp_dest, static_cast<T*>(a.out), a.tmp_dlow, cur2, w2, nb2, w1, c0 * w1 / kP2Tile);
+#ifndef BSG_P2_PERSISTENT
+#define BSG_P2_PERSISTENT 0
+#endif
+    if (BSG_P2_PERSISTENT) {
+      const size_t smp = kP2Tile * 2 * (sizeof(T) + 4);
+      cudaFuncSetAttribute(k_part2p<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smp));
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2p<T>, kP2Threads, smp);
+      const uint64_t ntiles = cn * w1 / kP2Tile;
+      const uint64_t g = std::min<uint64_t>(ntiles, static_cast<uint64_t>(sms) * std::max(per, 1));
+      k_part2p<T><<<static_cast<unsigned>(g), kP2Threads, smp, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
+                                                                      a.tmp_dlow, cur2, w2, nb2, w1,
+                                                                      c0 * w1 / kP2Tile, ntiles);
+    } else {
+      k_part2<T><<<static_cast<unsigned>(cn * w1 / kP2Tile), kP2Threads, sm2, s>>>(
+          tv, a.tmp_dest, static_cast<T*>(a.out), a.tmp_dlow, cur2, w2, nb2, w1, c0 * w1 / kP2Tile);
+    }
     k_place<T><<<static_cast<unsigned>(cn * w1 >> w2), kP3Threads, sm3, s>>>(
         static_cast<T*>(a.out), a.tmp_dlow, w2, c0 * w1 >> w2, BSG_PART_GROUP_MB > 0 ? 1 : 0);
     launched += 2;

@@ -512,3 +512,36 @@ def test_pipeline_with_pageable_buffers(bsg, cuda):
     with bsg.Pipeline(m, 8) as pipe:
         pipe.wait(pipe.submit(a, b, cfg_of(bsg, seed=31)))
     assert np.array_equal(b, O.shuffle_indices(m, 31))
+
+
+def test_pow2_wide_counters(bsg, cuda):
+    """m = 2^33 (64-bit counters on the all-survive path) on counter slices, both variants."""
+    from paper_2106_06161_b200 import _lib
+    m = 1 << 33
+    for variant in (PHILOX, LCG):
+        cfg = cfg_of(bsg, seed=0xC0FFEE, variant=variant)._c()
+        for a, b in ((0, 5000), ((1 << 32) - 2500, (1 << 32) + 2500), (m - 5000, m)):
+            out = cuda.empty(b - a, dtype=cuda.int64, device="cuda")
+            cnt = ctypes.c_uint64()
+            _lib.check(_lib.lib.bsg_shuffle_range(m, ctypes.byref(cfg), a, b, None, None, out.data_ptr(), 8,
+                                                  ctypes.addressof(cnt), None), "range")
+            assert cnt.value == b - a
+            exp = O.shuffle_indices_range(m, 0xC0FFEE, variant, 24, a, b)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), exp), (variant, a)
+
+
+def test_partitioned_512_coarse_buckets(bsg, cuda):
+    """2^30 u64 takes 512 coarse buckets (two bins per thread in P1's scan); equal to the single pass."""
+    m = 1 << 30
+    vals = cuda.arange(m, dtype=cuda.int64, device="cuda")
+    outs = []
+    for path in (2, 1):
+        old = bsg.set_path(path)
+        try:
+            outs.append(bsg.shuffle_values(vals, cfg_of(bsg, seed=30)))
+        finally:
+            bsg.set_path(old)
+    assert cuda.equal(outs[0], outs[1])
+    assert np.array_equal(outs[0][:4096].cpu().numpy().view(np.uint64), O.shuffle_indices_range(m, 30, PHILOX, 24, 0, 4096))
+    del vals, outs
+    cuda.cuda.empty_cache()
