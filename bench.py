@@ -318,8 +318,8 @@ def ours_arm(args, rank, world, local):
             for _ in range(max(2, e2e_steps // 2)):
                 bsg.shuffle_values_into(host_in, cfg, host_out)
             sync_ms = (time.perf_counter() - t1) / max(2, e2e_steps // 2) * 1e3
-            path = ("bsg_pipeline_submit/wait (C ABI): per step H2D of n*8 B from pinned host memory, fused shuffle "
-                    "kernel, D2H of n*8 B to pinned host memory; 3 streams, 2 device slots, so step i+1's H2D "
+            path = ("bsg_pipeline_submit/wait (C ABI): per step H2D of n*8 B from pinned host memory, the shuffle "
+                    "kernels, D2H of n*8 B to pinned host memory; 3 streams, 2 device slots, so step i+1's H2D "
                     "overlaps step i's D2H")
             sync = {"value": round(step_bytes_rank / (sync_ms * 1e-3) / 1e9, 3), "ms_per_step": round(sync_ms, 3),
                     "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call"}
@@ -400,8 +400,15 @@ def ours_arm(args, rank, world, local):
         "gpu_launches": int(launches),
         "e2e": e2e,
     }
+    if traffic:
+        # how close the kernels run to their own physical DRAM traffic at the measured peak
+        line["roofline"]["traffic_floor_ms"] = round(traffic / (peak * 1e9) * 1e3, 4)
+        line["roofline"]["frac_of_traffic_floor"] = round(traffic / (peak * 1e9) * 1e3 / kernel_ms, 4)
     if not args.no_comparators and world == 1 and not batch:
         line["comparators"] = comparators(bsg, torch, dev, vals, out, m_total, eb, cfg, stream)
+        gb = line["comparators"].get("gather_bound", {}).get("value")
+        if gb:
+            line["comparators"]["value_over_gather_bound"] = round(value / gb, 3)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, args.config)
     print(json.dumps(line), flush=True)
