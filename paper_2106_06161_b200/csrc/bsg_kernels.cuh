@@ -172,11 +172,18 @@ __device__ __forceinline__ unsigned long long pack_status(unsigned long long fla
   return flag | (static_cast<unsigned long long>(epoch & 0x3FFFFFu) << 40) | (v & kValMask);
 }
 
-// Warp 0: publish this tile's aggregate, walk back over predecessors 32 at a
-// time until an inclusive prefix is found, publish the inclusive prefix and
-// return the exclusive prefix (CUB-style decoupled look-back).
+// Warp 0: publish this tile's aggregate, then walk back over predecessors
+// 32*kLB at a time (each lane inspects kLB status words per round trip) until an
+// inclusive prefix is found; publish the inclusive prefix and return the
+// exclusive prefix (decoupled look-back).  Summing several
+// windows of aggregates per L2 round trip keeps small grids, where every tile
+// runs at once and inclusive prefixes lag, from serialising on the frontier.
+#ifndef BSG_LOOKBACK_PER_LANE
+#define BSG_LOOKBACK_PER_LANE 1
+#endif
 __device__ __forceinline__ unsigned long long lookback_warp(const Lookback& lb, uint32_t tile,
                                                             unsigned long long total) {
+  constexpr int kLB = BSG_LOOKBACK_PER_LANE;
   const int lane = threadIdx.x & 31;
   unsigned long long* st = lb.status;
   if (tile == 0) {
@@ -188,26 +195,45 @@ __device__ __forceinline__ unsigned long long lookback_warp(const Lookback& lb, 
   unsigned long long excl = 0;
   long long base = static_cast<long long>(tile) - 1;
   for (;;) {
-    const long long idx = base - lane;
-    unsigned long long w = 0;
-    unsigned flag = 2;  // lanes past tile 0 behave as an inclusive zero
-    if (idx >= 0) {
-      int spins = 0;
-      for (;;) {
-        w = ld_relaxed_gpu(st + idx);
-        flag = static_cast<unsigned>(w >> 62);
-        if (flag != 0 && static_cast<uint32_t>((w >> 40) & 0x3FFFFFu) == ep) break;
-        if (++spins > 8) __nanosleep(64);
+    unsigned long long w[kLB];
+    // Issue every load of the window first (one round trip), then re-poll only words not yet published.
+#pragma unroll
+    for (int q = 0; q < kLB; ++q) {
+      const long long idx = base - (lane + 32 * q);
+      w[q] = idx >= 0 ? ld_relaxed_gpu(st + idx) : pack_status(kFlagPre, lb.epoch, 0);
+    }
+    for (int spins = 0;; ++spins) {
+      bool ready = true;
+#pragma unroll
+      for (int q = 0; q < kLB; ++q)
+        ready &= (w[q] >> 62) != 0 && static_cast<uint32_t>((w[q] >> 40) & 0x3FFFFFu) == ep;
+      if (__all_sync(0xFFFFFFFFu, ready)) break;
+      if (spins > 8) __nanosleep(64);
+#pragma unroll
+      for (int q = 0; q < kLB; ++q) {
+        const long long idx = base - (lane + 32 * q);
+        const bool ok = (w[q] >> 62) != 0 && static_cast<uint32_t>((w[q] >> 40) & 0x3FFFFFu) == ep;
+        if (!ok && idx >= 0) w[q] = ld_relaxed_gpu(st + idx);
       }
     }
-    const unsigned pmask = __ballot_sync(0xFFFFFFFFu, flag == 2);
-    const int k = pmask ? __ffs(pmask) - 1 : 31;
-    unsigned long long v = (lane <= k && idx >= 0) ? (w & kValMask) : 0ULL;
+    unsigned long long val[kLB];
+    int nearest = 32 * kLB;  // smallest distance (lane + 32*q) holding an inclusive prefix
+#pragma unroll
+    for (int q = 0; q < kLB; ++q) {
+      val[q] = w[q] & kValMask;
+      if ((w[q] >> 62) == 2 && lane + 32 * q < nearest) nearest = lane + 32 * q;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nearest = min(nearest, __shfl_xor_sync(0xFFFFFFFFu, nearest, o));
+    unsigned long long v = 0;
+#pragma unroll
+    for (int q = 0; q < kLB; ++q)
+      if (lane + 32 * q <= nearest) v += val[q];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
     excl += v;
-    if (pmask) break;
-    base -= 32;
+    if (nearest < 32 * kLB) break;
+    base -= 32 * kLB;
   }
   if (lane == 0) st_relaxed_gpu(st + tile, pack_status(kFlagPre, lb.epoch, excl + total));
   return excl;
