@@ -201,11 +201,18 @@ def ours_arm(args, rank, world, local):
     import paper_2106_06161_b200 as bsg
     from paper_2106_06161_b200 import _lib
 
+    # BSG_BENCH_DEVICE / BSG_BENCH_BACKEND: debugging knobs to exercise the multi-rank code path with several
+    # ranks on one GPU (gloo); the driver's runs use one GPU per rank and NCCL.
+    local = int(os.environ.get("BSG_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BSG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     m_gpu, eb, variant, batch, desc = CONFIGS[args.config]
     cfg = bsg.ShuffleConfig(seed=SEED, variant=bsg.BijectionVariant(variant))
     stream = torch.cuda.current_stream(dev)
@@ -378,7 +385,8 @@ def ours_arm(args, rank, world, local):
     alg_bytes = step_bytes_rank  # per launch on this rank (one kernel per step)
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
     prof = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
-    traffic = prof.get(args.config, {}).get("dram_bytes_per_launch")
+    tkey = args.config + ("_single" if dominant == "bsg::k_pow2" and args.config == "c2" else "")
+    traffic = prof.get(tkey, {}).get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
