@@ -92,9 +92,11 @@ def test_philox_rejects_bad_parameters():  # unit_bijection.cpp:171-175
     y = ctypes.c_uint64()
     assert O.C.orc_philox_apply(8, k, 24, 256, ctypes.byref(y)) == -2  # out of domain
     for bits, rounds in [(1, 24), (64, 24), (8, 2)]:
-        out = np.empty(16, dtype=np.uint64)
-        assert O.C.orc_shuffle_indices(1 << min(bits, 4) | 3, 0, PHILOX, rounds, out.ctypes.data) in (0, -1)
-    assert O.C.orc_shuffle_indices(100, 0, PHILOX, 2, np.empty(100, dtype=np.uint64).ctypes.data) == -1
+        m = 1 << min(bits, 4) | 3
+        out = np.empty(m, dtype=np.uint64)  # room for every survivor the call may write
+        assert O.C.orc_shuffle_indices(m, 0, PHILOX, rounds, out.ctypes.data) in (0, -1)
+    out = np.empty(100, dtype=np.uint64)
+    assert O.C.orc_shuffle_indices(100, 0, PHILOX, 2, out.ctypes.data) == -1
 
 
 def test_domain_bits_table():  # unit_shuffle.cpp:39-46
