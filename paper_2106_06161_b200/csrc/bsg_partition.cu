@@ -9,7 +9,7 @@
 // permutation can be applied by streaming the INPUT in order and routing each
 // element by its destination f^-1(j) (philox_invert, bijection.hpp:117-143):
 //   P1  read in[] sequentially, inverse cipher -> dest, counting-sort each
-//       8192-element tile in shared memory into 2^s1 coarse destination
+//       4096-element tile in shared memory into 2^s1 coarse destination
 //       buckets, append the runs to the buckets (value + u32 dest);
 //   P2  per coarse bucket, the same split into 2^s2 fine windows of W2
 //       elements (value + u16 dest-in-window), written into `out` itself;
@@ -24,7 +24,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "bsg_kernels.cuh"
 #include "bsg_partition.h"
@@ -43,22 +42,16 @@ namespace {
 #define BSG_P2_THREADS 256
 #endif
 constexpr int kP1Threads = BSG_P1_THREADS, kP1Items = 4096 / BSG_P1_THREADS, kP1Tile = 4096;
-constexpr int kP2Threads = BSG_P2_THREADS, kP2Items = 4096 / BSG_P2_THREADS, kP2Tile = 4096;
+#ifndef BSG_P2_TILE
+#define BSG_P2_TILE 4096
+#endif
+constexpr int kP2Threads = BSG_P2_THREADS, kP2Items = BSG_P2_TILE / BSG_P2_THREADS, kP2Tile = BSG_P2_TILE;
+constexpr int kP2TileLog = __builtin_ctz(kP2Tile);  // coarse buckets must hold whole P2 tiles
 constexpr int kP3Threads = 512;
-#ifndef BSG_P23_THREADS
-#define BSG_P23_THREADS 512
-#endif
-constexpr int kP23Threads = BSG_P23_THREADS, kP23Items = kP2Tile / BSG_P23_THREADS;
-#ifndef BSG_PART_GROUP_MB
-#define BSG_PART_GROUP_MB 0
-#endif
-#ifndef BSG_PART_S1_BIAS
-#define BSG_PART_S1_BIAS 0
-#endif
+
 constexpr int kMaxB1 = 512, kMaxB2 = 256;
-// cursor region: P1 bucket cursors, P2 window cursors, fused-path completion counters + ticket
-constexpr int kMaxChunks = 16;
-constexpr size_t kCursorWords = kMaxB1 + static_cast<size_t>(kMaxB1) * kMaxB2 + kMaxB1 + 32 + kMaxChunks * kMaxB1;
+// cursor region: P1 bucket cursors, then P2 window cursors
+constexpr size_t kCursorWords = kMaxB1 + static_cast<size_t>(kMaxB1) * kMaxB2;
 
 constexpr int kKindDestArray = 100;  // destinations come from an array (scatter by permutation)
 
@@ -114,7 +107,7 @@ template <int KIND, int D, typename T>
 __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, T* __restrict__ tv,
                                                          uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
                                                          BijParams p, int bshift, int nb, uint64_t w1,
-                                                         const uint32_t* __restrict__ dsrc, uint32_t tile0) {
+                                                         const uint32_t* __restrict__ dsrc) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
   uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);
@@ -123,9 +116,9 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
   const int tid = threadIdx.x;
   for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
   __syncthreads();
-  const uint32_t base = (tile0 + blockIdx.x) * kP1Tile + tid;
+  const uint32_t base = blockIdx.x * kP1Tile + tid;
 #ifndef BSG_P1_LATE_LOAD
-#define BSG_P1_LATE_LOAD 1
+#define BSG_P1_LATE_LOAD 0
 #endif
   // Default: the input tile is loaded first (its latency hides under the cipher).  LATE_LOAD keeps the
   // values out of registers during the cipher (more resident CTAs) and loads them after the scan.
@@ -176,10 +169,9 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
 
 // P2: split each coarse bucket into fine windows of 2^w2 elements.
 template <typename T>
-__global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB) k_part2(const T* __restrict__ tv, const uint32_t* __restrict__ td,
-                                                         T* __restrict__ ov, uint16_t* __restrict__ od,
-                                                         uint32_t* __restrict__ cur2, int w2, int nb2,
-                                                         uint64_t w1, uint64_t tile_base, uint32_t swz) {
+__global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB)
+    k_part2(const T* __restrict__ tv, const uint32_t* __restrict__ td, T* __restrict__ ov, uint16_t* __restrict__ od,
+            uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
   uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
@@ -188,14 +180,7 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB) k
   const int tid = threadIdx.x;
   if (tid < nb2) hist[tid] = 0;
   __syncthreads();
-  // swz > 1: consecutive CTAs take tiles of different coarse buckets (swz buckets round-robin), so the CTAs
-  // resident at one time spread their cursor atomics over swz buckets instead of queueing on one bucket's.
-  uint64_t tile = blockIdx.x;
-  if (swz > 1) {
-    const uint64_t tpb = w1 / kP2Tile, grp = tile / (tpb * swz), k = tile % (tpb * swz);
-    tile = (grp * swz + k % swz) * tpb + k / swz;
-  }
-  const uint64_t t0 = (tile_base + tile) * kP2Tile;
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kP2Tile;
   const uint64_t coarse = t0 / w1;
   const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
   T v[kP2Items];
@@ -233,160 +218,14 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB) k
   }
 }
 
-// Chunked P2 (P1/P2 overlap): P1 runs over the input in K chunks; after
-// chunk k the coarse cursors are snapshotted, and chunk k's contribution to
-// coarse bucket b is the run [snap[k-1][b], snap[k][b]) of that bucket (P1
-// chunks append in launch order).  This kernel splits those runs while P1
-// computes the next chunk on another stream: P2 is bound by shared memory and
-// latency, P1 by the integer pipes, so the two overlap on the same SMs.
-template <typename T>
-__global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB) k_part2c(
-    const T* __restrict__ tv, const uint32_t* __restrict__ td, T* __restrict__ ov, uint16_t* __restrict__ od,
-    uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1, const uint32_t* __restrict__ snap_prev,
-    const uint32_t* __restrict__ snap, uint32_t tpc) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* sv = reinterpret_cast<T*>(smem);
-  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
-  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], wt[32];
-  __shared__ unsigned long long delta[kMaxB2];
-  const int tid = threadIdx.x;
-  const uint32_t coarse = blockIdx.x / tpc;
-  const uint32_t lo = snap_prev ? snap_prev[coarse] : 0u, hi = snap[coarse];
-  const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
-  uint32_t* cur = cur2 + static_cast<uint64_t>(coarse) * nb2;
-  const uint64_t win0 = static_cast<uint64_t>(coarse) * w1;
-  for (uint32_t t = lo + (blockIdx.x % tpc) * kP2Tile; t < hi; t += tpc * kP2Tile) {
-    const uint32_t nv = min(hi - t, static_cast<uint32_t>(kP2Tile));
-    const uint64_t t0 = win0 + t;
-    if (tid < nb2) hist[tid] = 0;
-    __syncthreads();
-    T v[kP2Items];
-    uint32_t d[kP2Items], rk[kP2Items];
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i) {
-      const uint32_t e = tid + i * kP2Threads;
-      if (e < nv) {
-        v[i] = __ldcs(tv + t0 + e);
-        d[i] = __ldcs(td + t0 + e);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i)
-      if (tid + i * kP2Threads < nv) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
-    __syncthreads();
-    scan_bins(hist, start, nb2, wt);
-    uint32_t g = 0;
-    if (tid < nb2) g = atomicAdd(cur + tid, hist[tid]);
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i)
-      if (tid + i * kP2Threads < nv) rk[i] += start[(d[i] >> w2) & fmask];
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i) {
-      if (tid + i * kP2Threads < nv) {
-        sv[rk[i]] = v[i];
-        sd[rk[i]] = d[i];
-      }
-    }
-    if (tid < nb2) delta[tid] = win0 + (static_cast<unsigned long long>(tid) << w2) + g - start[tid];
-    __syncthreads();
-    for (uint32_t q = tid; q < nv; q += kP2Threads) {
-      const uint32_t dd = sd[q];
-      const uint64_t pos = delta[(dd >> w2) & fmask] + q;
-      ov[pos] = sv[q];
-      od[pos] = static_cast<uint16_t>(dd & wmask);
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void k_snap(const uint32_t* __restrict__ cur, uint32_t* __restrict__ snap, int nb) {
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) snap[i] = cur[i];
-}
-
-// Persistent P2: each CTA loops over tiles; the next tile's values and
-// destinations stream into shared memory with cp.async while the current tile
-// is ranked, scattered and written, so the load latency leaves the critical path.
-template <typename T>
-__global__ void __launch_bounds__(kP2Threads) k_part2p(const T* __restrict__ tv, const uint32_t* __restrict__ td,
-                                                          T* __restrict__ ov, uint16_t* __restrict__ od,
-                                                          uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
-                                                          uint64_t tile_base, uint64_t ntiles) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* sv = reinterpret_cast<T*>(smem);
-  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
-  T* iv = reinterpret_cast<T*>(sd + kP2Tile);
-  uint32_t* id = reinterpret_cast<uint32_t*>(iv + kP2Tile);
-  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], wt[32];
-  __shared__ unsigned long long delta[kMaxB2];
-  const int tid = threadIdx.x;
-  const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
-  auto prefetch = [&](uint64_t t) {
-    const char* gv = reinterpret_cast<const char*>(tv + (tile_base + t) * kP2Tile);
-    const char* gd = reinterpret_cast<const char*>(td + (tile_base + t) * kP2Tile);
-    for (uint32_t o = tid * 16; o < kP2Tile * sizeof(T); o += kP2Threads * 16) {
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(reinterpret_cast<char*>(iv) + o));
-      asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst), "l"(gv + o) : "memory");
-    }
-    for (uint32_t o = tid * 16; o < kP2Tile * 4; o += kP2Threads * 16) {
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(reinterpret_cast<char*>(id) + o));
-      asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst), "l"(gd + o) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  uint64_t t = blockIdx.x;
-  if (t < ntiles) prefetch(t);
-  for (; t < ntiles; t += gridDim.x) {
-    if (tid < nb2) hist[tid] = 0;
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    T v[kP2Items];
-    uint32_t d[kP2Items], rk[kP2Items];
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i) {
-      v[i] = iv[tid + i * kP2Threads];
-      d[i] = id[tid + i * kP2Threads];
-    }
-    __syncthreads();  // input buffer free: stream the next tile in behind this one
-    if (t + gridDim.x < ntiles) prefetch(t + gridDim.x);
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
-    __syncthreads();
-    scan_bins(hist, start, nb2, wt);
-    const uint64_t t0 = (tile_base + t) * kP2Tile;
-    const uint64_t coarse = t0 / w1;
-    uint32_t* cur = cur2 + coarse * nb2;
-    const uint64_t win0 = coarse * w1;
-    if (tid < nb2)
-      delta[tid] =
-          win0 + (static_cast<unsigned long long>(tid) << w2) + atomicAdd(cur + tid, hist[tid]) - start[tid];
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i) {
-      const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
-      sv[s] = v[i];
-      sd[s] = d[i];
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int s = tid; s < kP2Tile; s += kP2Threads) {
-      const uint32_t dd = sd[s];
-      const uint64_t pos = delta[(dd >> w2) & fmask] + s;
-      ov[pos] = sv[s];
-      od[pos] = static_cast<uint16_t>(dd & wmask);
-    }
-    __syncthreads();  // staging reuse by the next tile
-  }
-}
-
 // P3: place each fine window through shared memory, in place in `out`.
 template <typename T>
-__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2,
-                                                      uint64_t win_base, int discard) {
+__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* win = reinterpret_cast<T*>(smem);
   const uint32_t W = 1u << w2;
-  T* o = out + ((win_base + blockIdx.x) << w2);
-  uint16_t* dd = od + ((win_base + blockIdx.x) << w2);
+  T* o = out + (static_cast<uint64_t>(blockIdx.x) << w2);
+  const uint16_t* dd = od + (static_cast<uint64_t>(blockIdx.x) << w2);
   constexpr int kU = 8;
   for (uint32_t i0 = threadIdx.x; i0 < W; i0 += kP3Threads * kU) {
     T v[kU];
@@ -404,157 +243,7 @@ __global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint1
       if (i0 + u * kP3Threads < W) win[d[u]] = v[u];
   }
   __syncthreads();
-  if (discard) {
-    // The window's u16 destinations are dead: drop their (L2-resident, dirty) lines without write-back.
-    for (uint32_t l = threadIdx.x; l < (W * 2) / 128; l += kP3Threads)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(dd) + l * 128) : "memory");
-  }
   for (uint32_t i = threadIdx.x; i < W; i += kP3Threads) __stcs(o + i, win[i]);
-}
-
-// Fused, persistent P2+P3 with L2 hand-off.  One ticketed work list covers
-// both passes: phase b holds the P2 tiles of coarse bucket b interleaved
-// (r : 1, r = tiles per window) with the P3 windows of bucket b - lag.  A
-// bucket's fine windows are therefore placed while its P2 output (values +
-// u16 destinations, ~10 B/element) is still resident in L2: P3 reads them
-// from L2, drops the dead destination lines without write-back, and the value
-// lines are overwritten in place, so DRAM sees 12 B/element read + 8 B
-// written for both passes instead of 22 + 18.  A P3 item only waits for P2
-// tiles with smaller tickets, which running CTAs already own: no deadlock.
-struct P23Args {
-  uint32_t* cur2;    // nb1 * nb2 fine-window append cursors
-  uint32_t* done;    // nb1 finished-P2-tile counters
-  uint32_t* ticket;  // work-list ticket (first gridDim.x items are implicit)
-  uint64_t w1;       // elements per coarse bucket
-  uint32_t tp, wp;   // P2 tiles and P3 windows per coarse bucket
-  uint32_t r;        // tp / wp
-  uint32_t nb1, lag, nitems;
-  int w2, nb2;
-};
-
-struct P23Item {
-  uint32_t kind;  // 0 = P2 tile, 1 = P3 window
-  uint32_t bucket, index;
-};
-
-__device__ __forceinline__ P23Item p23_decode(uint32_t t, const P23Args& a) {
-  const uint32_t head = a.lag * a.tp, phase = a.tp + a.wp, mid = (a.nb1 - a.lag) * phase;
-  if (t < head) return {0u, t / a.tp, t % a.tp};
-  t -= head;
-  if (t < mid) {
-    const uint32_t b = a.lag + t / phase, k = t % phase, g = k / (a.r + 1), j = k % (a.r + 1);
-    if (j < a.r) return {0u, b, g * a.r + j};
-    return {1u, b - a.lag, g};
-  }
-  t -= mid;
-  return {1u, a.nb1 - a.lag + t / a.wp, t % a.wp};
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kP23Threads, 2) k_part23(const T* __restrict__ tv, const uint32_t* __restrict__ td,
-                                                          T* __restrict__ out, uint16_t* __restrict__ od, P23Args a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t hist[kMaxB2], start[kMaxB2], wt[32];
-  __shared__ unsigned long long delta[kMaxB2];
-  __shared__ uint32_t s_next[2];
-  const int tid = threadIdx.x;
-  const int w2 = a.w2, nb2 = a.nb2;
-  const uint32_t fmask = static_cast<uint32_t>(nb2 - 1), wmask = (1u << w2) - 1;
-  uint32_t t = blockIdx.x, par = 0, pend = 0;
-  while (t < a.nitems) {
-    // claim ahead (its latency hides under this item); two slots so a slow reader of the previous claim never
-    // sees this one
-    if (tid == 0) {
-      s_next[par] = gridDim.x + atomicAdd(a.ticket, 1u);
-      if (pend) {
-        // Release the previous P2 tile: the block barrier that ended it orders every thread's stores before
-        // this thread's fence (cumulativity, as in a grid barrier); deferring it to here lets the other warps
-        // start this item instead of all waiting for the stores to drain.
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.done + pend - 1) : "memory");
-      }
-    }
-    pend = 0;
-    const P23Item it = p23_decode(t, a);
-    if (it.kind == 0) {
-      T* sv = reinterpret_cast<T*>(smem);
-      uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);
-      if (tid < nb2) hist[tid] = 0;
-      const uint64_t t0 = static_cast<uint64_t>(it.bucket) * a.w1 + static_cast<uint64_t>(it.index) * kP2Tile;
-      T v[kP23Items];
-      uint32_t d[kP23Items], rk[kP23Items];
-#pragma unroll
-      for (int i = 0; i < kP23Items; ++i) {
-        v[i] = __ldcs(tv + t0 + tid + i * kP23Threads);
-        d[i] = __ldcs(td + t0 + tid + i * kP23Threads);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int i = 0; i < kP23Items; ++i) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
-      __syncthreads();
-      scan_bins(hist, start, nb2, wt);
-      uint32_t* cur = a.cur2 + static_cast<uint64_t>(it.bucket) * nb2;
-      const uint64_t win0 = static_cast<uint64_t>(it.bucket) * a.w1;
-      uint32_t g = 0;
-      if (tid < nb2) g = atomicAdd(cur + tid, hist[tid]);  // consumed after the scatter (latency hidden)
-#pragma unroll
-      for (int i = 0; i < kP23Items; ++i) rk[i] += start[(d[i] >> w2) & fmask];
-#pragma unroll
-      for (int i = 0; i < kP23Items; ++i) {
-        sv[rk[i]] = v[i];
-        sd[rk[i]] = d[i];
-      }
-      if (tid < nb2) delta[tid] = win0 + (static_cast<unsigned long long>(tid) << w2) + g - start[tid];
-      __syncthreads();
-#pragma unroll 4
-      for (int s = tid; s < kP2Tile; s += kP23Threads) {
-        const uint32_t dd = sd[s];
-        const uint64_t pos = delta[(dd >> w2) & fmask] + s;
-        out[pos] = sv[s];  // default write-back policy: stays in L2 for the P3 of this bucket
-        od[pos] = static_cast<uint16_t>(dd & wmask);
-      }
-      pend = it.bucket + 1;  // published by thread 0 at the top of the next item (see there)
-    } else {
-      T* win = reinterpret_cast<T*>(smem);
-      if (tid == 0) {
-        const uint32_t* flag = a.done + it.bucket;
-        uint32_t c;
-        while (true) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(flag) : "memory");
-          if (c >= a.tp) break;
-          __nanosleep(256);
-        }
-      }
-      __syncthreads();
-      const uint32_t W = 1u << w2;
-      const uint64_t w0 = (static_cast<uint64_t>(it.bucket) * a.wp + it.index) << w2;
-      T* o = out + w0;
-      uint16_t* dd = od + w0;
-      constexpr int kU = sizeof(T) <= 8 ? 4 : 2;
-      for (uint32_t i0 = tid; i0 < W; i0 += kP23Threads * kU) {
-        T v[kU];
-        uint16_t d[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const uint32_t i = i0 + u * kP23Threads;
-          if (i < W) {
-            v[u] = __ldcg(o + i);
-            d[u] = __ldcg(reinterpret_cast<const unsigned short*>(dd) + i);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (i0 + u * kP23Threads < W) win[d[u]] = v[u];
-      }
-      __syncthreads();
-      for (uint32_t l = tid; l < (W * 2) / 128; l += kP23Threads)
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(dd) + l * 128) : "memory");
-      for (uint32_t i = tid; i < W; i += kP23Threads) __stcs(o + i, win[i]);
-    }
-    __syncthreads();  // s_next visible; shared staging free for the next item
-    t = s_next[par];
-    par ^= 1;
-  }
-  if (tid == 0 && pend) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.done + pend - 1) : "memory");
 }
 
 template <typename T>
@@ -562,174 +251,38 @@ int window_log2() {
   return sizeof(T) == 4 ? 14 : (sizeof(T) == 8 ? 13 : 12);  // 64 KiB smem window
 }
 
-// Runtime knobs (read once): BSG_P23=0 selects the separate P2/P3 kernels; BSG_P23_LAG is the bucket lag of
-// the fused list; BSG_P23_S2 the fine fan-out (log2) the fused path prefers.
-struct PartKnobs {
-  int fused = 0, lag = 2, s2 = 7, swz = 1, chunks = 1, prio = 1;
-  PartKnobs() {
-    if (const char* e = std::getenv("BSG_PART_CHUNKS")) chunks = std::max(1, std::min(kMaxChunks, std::atoi(e)));
-    if (const char* e = std::getenv("BSG_PART_PRIO")) prio = std::atoi(e);
-    if (const char* e = std::getenv("BSG_P2_SWZ")) swz = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("BSG_P23")) fused = std::atoi(e);
-    if (const char* e = std::getenv("BSG_P23_LAG")) lag = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("BSG_P23_S2")) s2 = std::atoi(e);
-  }
-};
-const PartKnobs& knobs() {
-  static const PartKnobs k;
-  return k;
-}
-
 // Coarse/fine split of the bits above the window: (s1, s2) fan-outs.
-void part_split(int bits, int w2, bool fused, int& s1, int& s2) {
+void part_split(int bits, int w2, int& s1, int& s2) {
   const int total = bits - w2;
-  s1 = (total + 1) / 2 + BSG_PART_S1_BIAS;
+  s1 = (total + 1) / 2;
   s2 = total - s1;
-  if (fused) {
-    const int want2 = knobs().s2, t1 = total - want2;
-    if (want2 >= 1 && t1 >= 1 && (1 << t1) <= kMaxB1 && (1 << want2) <= kMaxB2 && bits - t1 >= 12) {
-      s1 = t1;
-      s2 = want2;
-    }
-  }
-}
-
-// Per-device auxiliary stream (high priority, so P2 blocks are dispatched ahead of queued P1 blocks) and the
-// events of the chunked P1/P2 overlap.  Calls on one device are serialised by the caller's context lock.
-struct AuxStreams {
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev[kMaxChunks] = {};
-  cudaEvent_t join = nullptr;
-  bool ok = false;
-};
-AuxStreams& aux_streams() {
-  static AuxStreams per_dev[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  AuxStreams& x = per_dev[dev & 63];
-  if (!x.ok) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    bool good = cudaStreamCreateWithPriority(&x.aux, cudaStreamNonBlocking, knobs().prio ? hi : lo) == cudaSuccess;
-    for (int k = 0; k < kMaxChunks && good; ++k)
-      good = cudaEventCreateWithFlags(&x.ev[k], cudaEventDisableTiming) == cudaSuccess;
-    good = good && cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) == cudaSuccess;
-    x.ok = good;
-  }
-  return x;
 }
 
 template <int KIND, int D, typename T>
 cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   const int b = a.p.bits;
   const int w2 = window_log2<T>();
-  const bool fused = knobs().fused != 0 && BSG_PART_GROUP_MB == 0;
   int s1, s2;
-  part_split(b, w2, fused, s1, s2);
+  part_split(b, w2, s1, s2);
   const uint64_t n = 1ULL << b, w1 = 1ULL << (b - s1);
   const int nb1 = 1 << s1, nb2 = 1 << s2;
   uint32_t* cur1 = a.cursors;
   uint32_t* cur2 = a.cursors + nb1;
-  uint32_t* done = a.cursors + kMaxB1 + kMaxB1 * kMaxB2;  // fused path: per-bucket P2 completion, then ticket
   cudaError_t e = cudaMemsetAsync(a.cursors, 0, kCursorWords * 4, s);
   if (e != cudaSuccess) return e;
   const size_t sm1 = kP1Tile * (sizeof(T) + 4);
   const size_t sm2 = kP2Tile * (sizeof(T) + 4);
   const size_t sm3 = (size_t{1} << w2) * sizeof(T);
   cudaFuncSetAttribute(k_part1<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
-  T* tv = static_cast<T*>(a.tmp_values);
-  const int K = fused ? 1 : static_cast<int>(std::min<uint64_t>(knobs().chunks, n / kP1Tile));
-  if (K > 1) {
-    // P1 in K chunks on `s`; chunk k's P2 on an auxiliary stream as soon as its cursors are snapshotted.
-    uint32_t* snap = done + kMaxB1 + 32;
-    AuxStreams& x = aux_streams();
-    if (!x.ok) return cudaErrorNotReady;
-    const uint64_t tiles = n / kP1Tile, per = tiles / K;
-    cudaFuncSetAttribute(k_part2c<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
-    const uint32_t tpc = static_cast<uint32_t>(w1 / K / kP2Tile + 1);
-    for (int k = 0; k < K; ++k) {
-      const uint64_t t0 = per * k, nt = (k == K - 1) ? tiles - t0 : per;
-      k_part1<KIND, D, T><<<static_cast<unsigned>(nt), kP1Threads, sm1, s>>>(
-          static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in,
-          static_cast<uint32_t>(t0));
-      k_snap<<<1, 512, 0, s>>>(cur1, snap + k * kMaxB1, nb1);
-      cudaEventRecord(x.ev[k], s);
-      cudaStreamWaitEvent(x.aux, x.ev[k], 0);
-      k_part2c<T><<<static_cast<unsigned>(nb1 * tpc), kP2Threads, sm2, x.aux>>>(
-          tv, a.tmp_dest, static_cast<T*>(a.out), a.tmp_dlow, cur2, w2, nb2, w1,
-          k ? snap + (k - 1) * kMaxB1 : nullptr, snap + k * kMaxB1, tpc);
-    }
-    cudaEventRecord(x.join, x.aux);
-    cudaStreamWaitEvent(s, x.join, 0);
-    cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
-    k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2, 0,
-                                                                       0);
-    note_launch(3 * K + 1);
-    return cudaGetLastError();
-  }
-  k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
-      static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, 0u);
-  if (fused) {
-    const size_t sm23 = std::max(sm2, sm3);
-    cudaFuncSetAttribute(k_part23<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm23));
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part23<T>, kP23Threads, sm23);
-    P23Args g;
-    g.cur2 = cur2;
-    g.done = done;
-    g.ticket = done + kMaxB1;
-    g.w1 = w1;
-    g.tp = static_cast<uint32_t>(w1 / kP2Tile);
-    g.wp = static_cast<uint32_t>(w1 >> w2);
-    g.r = g.tp / g.wp;
-    g.nb1 = static_cast<uint32_t>(nb1);
-    g.lag = static_cast<uint32_t>(std::min(knobs().lag, nb1 - 1));
-    g.nitems = static_cast<uint32_t>(nb1) * (g.tp + g.wp);
-    g.w2 = w2;
-    g.nb2 = nb2;
-    const uint32_t grid = std::min<uint32_t>(g.nitems, static_cast<uint32_t>(sms) * std::max(per, 1));
-    k_part23<T><<<grid, kP23Threads, sm23, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out), a.tmp_dlow, g);
-    note_launch(2);
-    return cudaGetLastError();
-  }
   cudaFuncSetAttribute(k_part2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
   cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
-  // Grouped mode: P2 and P3 alternate over groups of coarse buckets sized to stay resident in L2, so P3
-  // reads P2's output from L2 and its dead destination lines are discarded instead of written back.
-  const uint64_t bucket_bytes = w1 * (sizeof(T) + 2);
-  const uint64_t group = BSG_PART_GROUP_MB > 0
-                             ? std::max<uint64_t>(1, (static_cast<uint64_t>(BSG_PART_GROUP_MB) << 20) / bucket_bytes)
-                             : static_cast<uint64_t>(nb1);
-  uint64_t launched = 1;
-  for (uint64_t c0 = 0; c0 < static_cast<uint64_t>(nb1); c0 += group) {
-    const uint64_t cn = std::min<uint64_t>(group, nb1 - c0);
-#ifndef BSG_P2_PERSISTENT
-#define BSG_P2_PERSISTENT 0
-#endif
-    if (BSG_P2_PERSISTENT) {
-      const size_t smp = kP2Tile * 2 * (sizeof(T) + 4);
-      cudaFuncSetAttribute(k_part2p<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smp));
-      int dev = 0, sms = 148, per = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2p<T>, kP2Threads, smp);
-      const uint64_t ntiles = cn * w1 / kP2Tile;
-      const uint64_t g = std::min<uint64_t>(ntiles, static_cast<uint64_t>(sms) * std::max(per, 1));
-      k_part2p<T><<<static_cast<unsigned>(g), kP2Threads, smp, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
-                                                                      a.tmp_dlow, cur2, w2, nb2, w1,
-                                                                      c0 * w1 / kP2Tile, ntiles);
-    } else {
-      k_part2<T><<<static_cast<unsigned>(cn * w1 / kP2Tile), kP2Threads, sm2, s>>>(
-          tv, a.tmp_dest, static_cast<T*>(a.out), a.tmp_dlow, cur2, w2, nb2, w1, c0 * w1 / kP2Tile,
-          static_cast<uint32_t>(std::min<uint64_t>(knobs().swz, cn)));
-    }
-    k_place<T><<<static_cast<unsigned>(cn * w1 >> w2), kP3Threads, sm3, s>>>(
-        static_cast<T*>(a.out), a.tmp_dlow, w2, c0 * w1 >> w2, BSG_PART_GROUP_MB > 0 ? 1 : 0);
-    launched += 2;
-  }
-  note_launch(launched);
+  T* tv = static_cast<T*>(a.tmp_values);
+  k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
+      static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in);
+  k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
+                                                                          a.tmp_dlow, cur2, w2, nb2, w1);
+  k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2);
+  note_launch(3);
   return cudaGetLastError();
 }
 
@@ -913,10 +466,10 @@ bool partition_eligible(int elem_code, int bits) {
     default: return false;
   }
   const int total = bits - w2;
-  const int s1 = (total + 1) / 2 + BSG_PART_S1_BIAS, s2 = total - s1;
+  const int s1 = (total + 1) / 2, s2 = total - s1;
   // fan-outs within the shared-memory histograms; tiles must not straddle buckets; 32-bit destinations
   return bits <= 32 && s1 >= 1 && s2 >= 1 && (1 << s1) <= kMaxB1 && (1 << s2) <= kMaxB2 &&
-         (bits - s1) >= 12 && bits >= 14;
+         (bits - s1) >= kP2TileLog && bits >= 14;
 }
 
 size_t partition_workspace_bytes(int elem_code, int bits) {

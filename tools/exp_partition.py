@@ -1,4 +1,5 @@
-"""Partitioned path variants (env knobs BSG_P23, BSG_P23_LAG, BSG_P23_S2) vs the single pass: equality + time."""
+"""Partitioned path (set_path(2)) vs the single pass: bit equality and time per case.  BSG_LIB selects a variant
+build (tools/run_var.sh); the first argument limits the number of cases."""
 import os
 import sys
 
@@ -20,7 +21,7 @@ def t(fn, reps=5):
     return a.elapsed_time(b) / reps
 
 
-tag = " ".join(f"{k}={os.environ[k]}" for k in ("BSG_P23", "BSG_P23_LAG", "BSG_P23_S2", "BSG_PART_CHUNKS", "BSG_PART_PRIO", "BSG_LIB") if k in os.environ)
+tag = " ".join(f"{k}={os.environ[k]}" for k in ("BSG_LIB",) if k in os.environ)
 cases = [(29, torch.int64, 1), (29, torch.int64, 0), (28, torch.int32, 1), (24, torch.int64, 1), (20, torch.int64, 1),
          (16, torch.int64, 1), (14, torch.int32, 1), (26, torch.complex128, 1)]
 if len(sys.argv) > 1:
