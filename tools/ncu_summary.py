@@ -35,11 +35,20 @@ KEYS = [
 
 
 def short_name(k: str) -> str:
-    m = re.search(r"bsg::(\w+)", k)
-    if m:
-        return "bsg::" + m.group(1)
-    m = re.search(r"(\w+)(<|\()", k)
-    return (m.group(1) if m else k)[:60]
+    """Kernel name without template arguments and parameter list: 'void bsg::<unnamed>::k_part1<2, 1, ...>(...)'
+    -> 'bsg::k_part1'."""
+    head = re.sub(r"(<unnamed>|\(anonymous namespace\)|^void unnamed>|unnamed>)::", "", k.split("(")[0])
+    bsg = "bsg::" in head or "k_" in head  # raw-page names lose the namespace prefix
+    depth, base = 0, ""
+    for ch in head:  # drop template argument lists
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        elif depth == 0:
+            base += ch
+    name = base.replace("void ", "").strip().split("::")[-1]
+    return ("bsg::" + name if bsg and name.startswith("k_") else name)[:60]
 
 
 def launches(path: str):
@@ -85,7 +94,7 @@ def raw_metrics_row(hdr, units, vals):
                 pass
     tot = sum(s for s, _ in stalls) or 1.0
     res["stall_pct"] = {n: round(100 * s / tot, 1) for s, n in sorted(stalls, reverse=True)[:8]}
-    res["kernel"] = short_name(d.get("Kernel Name", ("", ""))[0]).replace("bsg::<unnamed>", "bsg")
+    res["kernel"] = short_name(d.get("Kernel Name", ("", ""))[0])
     return res
 
 
