@@ -34,7 +34,19 @@ CONFIGS = {
     "c2lcg": (1 << 29, 8, 0, 0, "C2: n=2^29 uint64, power-of-two domain, LCG"),
     "c1": (1 << 20, 8, 1, 0, "C1: n=2^20 uint64, VariablePhilox-24"),
     "c4": (1024, 4, 1, 8192, "C4: 8192 shuffles of n=1024 uint32 per GPU (65536 over 8), VariablePhilox-24"),
+    "c5": (1 << 30, 16, 1, 0, "C5: 16-byte {u64 key, u64 value} records, 2^30 per GPU (n=2^33 over 8 GPUs), "
+                              "VariablePhilox-24"),
 }
+DTYPES = {4: "u32", 8: "u64", 16: "u64x2 (key+value record)"}
+
+
+def make_values(torch, n, eb, device=None, pin=False):
+    """Synthetic payload: iota for 4/8-byte elements; {key=2i, value=2i+1} records for 16-byte ones."""
+    if eb == 16:
+        t = torch.arange(2 * n, dtype=torch.int64, device=device).view(torch.complex128)
+    else:
+        t = torch.arange(n, dtype={4: torch.int32, 8: torch.int64}[eb], device=device)
+    return t.pin_memory() if pin else t
 
 
 def parse():
@@ -145,6 +157,13 @@ def reference_arm(args, rank, world):
             t_all.append(time.perf_counter() - t0)
         times = t_all[args.warmup:]
         bytes_step = 2 * batch * m * eb
+    elif eb == 16:
+        m_sample = min(m, 1 << 28)
+        note = f"{m_sample} 16-byte records per step (of the {m} per GPU)"
+        rc = O.REF.ref_time_shuffle_pairs_calls(m_sample, SEED, variant, 24, 0, calls, per)
+        assert rc == 0, rc
+        times = list(per)[args.warmup:]
+        bytes_step = 2 * m_sample * 16
     else:
         rc = O.REF.ref_time_shuffle_u64_calls(m_sample, SEED, variant, 24, 0, calls, per, ctypes.byref(fnv))
         assert rc == 0, rc
@@ -156,12 +175,12 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64" if eb == 8 else "u32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[eb],
         "data": "synthetic (iota values)",
         "config": {"workload": desc + (f" (reference sample: {note})"), "n": m_sample, "elem_bytes": eb,
                    "seed": SEED, "rounds": 24, "variant": "VariablePhilox" if variant else "Lcg"},
         "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"n={m_sample} u64 per step ({note}); {os.path.basename(O.REF.path)}, "
+                         "sample": f"n={m_sample} {DTYPES[eb]} per step ({note}); {os.path.basename(O.REF.path)}, "
                                    f"avx512={bool(O.REF.ref_avx512_active())}, workers=0 (all host threads)"},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -188,6 +207,16 @@ def cpu_baseline_leg(args, cfgname):
     if batch:
         return None
     trials = 3 if m >= (1 << 26) else 5
+    if eb == 16:
+        import ctypes
+        ms = min(m, 1 << 28)
+        per = (ctypes.c_double * (trials + 1))()
+        assert O.REF.ref_time_shuffle_pairs_calls(ms, SEED, variant, 24, 0, trials + 1, per) == 0
+        mean = sum(list(per)[1:]) / trials
+        return {"value": round(2 * ms * 16 / mean / 1e9, 3), "unit": "GB/s",
+                "cores": int(O.REF.ref_hardware_threads()), "kind": "reference",
+                "sample": f"n={ms} 16-byte records (bench.hpp:112-114 Pair), 1 warm-up + mean of {trials}, "
+                          f"{os.path.basename(O.REF.path)}, avx512={bool(O.REF.ref_avx512_active())}"}
     mean, _ = O.ref_time_shuffle_u64(m, SEED, variant, 24, trials)
     return {"value": round(2 * m * 8 / mean / 1e9, 3), "unit": "GB/s", "cores": int(O.REF.ref_hardware_threads()),
             "kind": "reference",
@@ -216,7 +245,7 @@ def ours_arm(args, rank, world, local):
     m_gpu, eb, variant, batch, desc = CONFIGS[args.config]
     cfg = bsg.ShuffleConfig(seed=SEED, variant=bsg.BijectionVariant(variant))
     stream = torch.cuda.current_stream(dev)
-    tdt = {4: torch.int32, 8: torch.int64}[eb]
+    tdt = {4: torch.int32, 8: torch.int64, 16: torch.complex128}[eb]
 
     if batch:
         m_total = m_gpu
@@ -230,7 +259,7 @@ def ours_arm(args, rank, world, local):
         dominant = "bsg::k_batched"
     else:
         m_total = m_gpu * world  # weak scaling: one global shuffle of N * n elements
-        vals = torch.arange(m_total, dtype=tdt, device=dev)  # replicated input
+        vals = make_values(torch, m_total, eb, device=dev)  # replicated input
         step_bytes_rank = 2 * m_gpu * eb
         if world == 1:
             out = torch.empty(m_total, dtype=tdt, device=dev)
@@ -303,21 +332,25 @@ def ours_arm(args, rank, world, local):
     e2e_steps = args.e2e_steps or min(args.steps, 6)
     if not batch:
         if world == 1:
-            pairs = [(torch.arange(m_total, dtype=tdt).pin_memory(), torch.empty(m_total, dtype=tdt).pin_memory())
-                     for _ in range(2)]
+            # two host (in, out) pairs so step i+1 never touches step i's buffers; one pair for 16-byte records
+            # (2 x 16 GiB pinned), where consecutive steps write the same output bytes
+            pairs = [(make_values(torch, m_total, eb, pin=True), torch.empty(m_total, dtype=tdt).pin_memory())
+                     for _ in range(1 if eb == 16 else 2)]
             h2d, d2h = m_total * eb, m_total * eb
             with bsg.Pipeline(m_total, eb, depth=2) as pipe:
-                tk = [pipe.submit(pairs[i % 2][0], pairs[i % 2][1], cfg) for i in range(2)]  # warm-up
+                P = len(pairs)
+                tk = [pipe.submit(pairs[i % P][0], pairs[i % P][1], cfg) for i in range(2)]  # warm-up
                 for x in tk:
                     pipe.wait(x)
                 t0 = time.perf_counter()
-                tk = [pipe.submit(pairs[i % 2][0], pairs[i % 2][1], cfg) for i in range(e2e_steps)]
+                tk = [pipe.submit(pairs[i % P][0], pairs[i % P][1], cfg) for i in range(e2e_steps)]
                 for x in tk:
                     pipe.wait(x)
                 el = time.perf_counter() - t0
             # result check of the last step against the device path
             ref = bsg.shuffle_values(vals, cfg).cpu()
-            assert torch.equal(pairs[(e2e_steps - 1) % 2][1], ref), "e2e output mismatch"
+            assert torch.equal(pairs[(e2e_steps - 1) % P][1].view(torch.int64), ref.view(torch.int64)), \
+                "e2e output mismatch"
             del ref
             host_in, host_out = pairs[0]
             bsg.shuffle_values_into(host_in, cfg, host_out)
@@ -325,9 +358,9 @@ def ours_arm(args, rank, world, local):
             for _ in range(max(2, e2e_steps // 2)):
                 bsg.shuffle_values_into(host_in, cfg, host_out)
             sync_ms = (time.perf_counter() - t1) / max(2, e2e_steps // 2) * 1e3
-            path = ("bsg_pipeline_submit/wait (C ABI): per step H2D of n*8 B from pinned host memory, the shuffle "
-                    "kernels, D2H of n*8 B to pinned host memory; 3 streams, 2 device slots, so step i+1's H2D "
-                    "overlaps step i's D2H")
+            path = (f"bsg_pipeline_submit/wait (C ABI): per step H2D of n*{eb} B from pinned host memory, the "
+                    f"shuffle kernels, D2H of n*{eb} B to pinned host memory; 3 streams, 2 device slots, so step "
+                    "i+1's H2D overlaps step i's D2H")
             sync = {"value": round(step_bytes_rank / (sync_ms * 1e-3) / 1e9, 3), "ms_per_step": round(sync_ms, 3),
                     "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call"}
             del pairs
@@ -337,7 +370,7 @@ def ours_arm(args, rank, world, local):
             # (bsg_scatter_permutation); each rank reads back its output shard.
             from paper_2106_06161_b200 import distributed as D
             S = m_total // world
-            host_in = (torch.arange(rank * S, (rank + 1) * S, dtype=tdt)).pin_memory()
+            host_in = make_values(torch, m_total, eb)[rank * S:(rank + 1) * S].clone().pin_memory()
             host_out = torch.empty(S, dtype=tdt).pin_memory()
             dev_in = torch.empty(S, dtype=tdt, device=dev)
 
@@ -391,13 +424,13 @@ def ours_arm(args, rank, world, local):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64" if eb == 8 else "u32", "data": "synthetic (iota values, device-generated)",
+        "vs_baseline": None, "dtype": DTYPES[eb], "data": "synthetic (iota values, device-generated)",
         "config": {"workload": desc + ("" if world == 1 else f"; global shuffle of {world}x n elements, "
                                                              "counter-range partition, replicated input"),
                    "n_per_gpu": m_gpu, "n_total": m_total if not batch else batch * m_gpu * world,
                    "elem_bytes": eb, "seed": SEED, "rounds": 24,
                    "variant": "VariablePhilox" if variant else "Lcg",
-                   "l2": "inputs (>= 4 GiB) exceed the 126 MB L2; no flush" if not batch
+                   "l2": f"inputs ({m_total * eb >> 30} GiB) exceed the 126 MB L2; no flush" if not batch
                    else "256 MiB per step > L2; no flush",
                    "parallelism": f"counter-range partition x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 3), "peak": peak,

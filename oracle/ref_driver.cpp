@@ -188,4 +188,24 @@ int ref_time_shuffle_u64_calls(uint64_t m, uint64_t seed, int variant, int round
   });
 }
 
+// C5 payload: 16-byte {u64 key, u64 value} records (the Pair of bench.hpp:112-114),
+// keys = i, values = ~i; each call timed individually as above.
+int ref_time_shuffle_pairs_calls(uint64_t m, uint64_t seed, int variant, int rounds, int workers, int calls,
+                                 double* per_call_s) {
+  struct Pair {
+    uint64_t key, value;
+  };
+  return guarded([&] {
+    const ShuffleConfig cfg = make_cfg(seed, variant, rounds, workers);
+    auto values = detail::make_buffer<Pair>(m);
+    for (uint64_t i = 0; i < m; ++i) values[i] = Pair{i, ~i};
+    auto out = detail::make_buffer<Pair>(m);
+    for (int t = 0; t < calls; ++t) {
+      const double t0 = now_s();
+      shuffle_values_into(values, cfg, out);
+      per_call_s[t] = now_s() - t0;
+    }
+  });
+}
+
 }  // extern "C"

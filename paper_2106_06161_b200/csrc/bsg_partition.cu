@@ -35,9 +35,6 @@ namespace {
 #ifndef BSG_P1_THREADS
 #define BSG_P1_THREADS 256
 #endif
-#ifndef BSG_P2_MINB
-#define BSG_P2_MINB 3
-#endif
 #ifndef BSG_P2_THREADS
 #define BSG_P2_THREADS 256
 #endif
@@ -49,7 +46,7 @@ constexpr int kP2Threads = BSG_P2_THREADS, kP2Items = BSG_P2_TILE / BSG_P2_THREA
 constexpr int kP2TileLog = __builtin_ctz(kP2Tile);  // coarse buckets must hold whole P2 tiles
 constexpr int kP3Threads = 512;
 
-constexpr int kMaxB1 = 512, kMaxB2 = 256;
+constexpr int kMaxB1 = 512, kMaxB2 = 512;  // fan-outs: at most 2 bins per thread in the scans
 // cursor region: P1 bucket cursors, then P2 window cursors
 constexpr size_t kCursorWords = kMaxB1 + static_cast<size_t>(kMaxB1) * kMaxB2;
 
@@ -169,7 +166,7 @@ __global__ void __launch_bounds__(kP1Threads) k_part1(const T* __restrict__ in, 
 
 // P2: split each coarse bucket into fine windows of 2^w2 elements.
 template <typename T>
-__global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB)
+__global__ void __launch_bounds__(kP2Threads, sizeof(T) <= 8 ? 3 : 2)
     k_part2(const T* __restrict__ tv, const uint32_t* __restrict__ td, T* __restrict__ ov, uint16_t* __restrict__ od,
             uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -179,6 +176,7 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB)
   __shared__ unsigned long long delta[kMaxB2];
   const int tid = threadIdx.x;
   if (tid < nb2) hist[tid] = 0;
+  if (tid + kP2Threads < nb2) hist[tid + kP2Threads] = 0;  // nb2 <= 2 * kP2Threads
   __syncthreads();
   const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kP2Tile;
   const uint64_t coarse = t0 / w1;
@@ -196,18 +194,19 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) > 8 ? 2 : BSG_P2_MINB)
   scan_bins(hist, start, nb2, wt);
   uint32_t* cur = cur2 + coarse * nb2;
   const uint64_t win0 = coarse * w1;  // first element of this coarse bucket's output range
-  // The cursor atomics are issued here and consumed after the shared-memory scatter, which hides their
-  // round trip; the slots are all read before any scatter store (no false LDS->STS ordering).
-  uint32_t g = 0;
-  if (tid < nb2) g = atomicAdd(cur + tid, hist[tid]);
-#pragma unroll
-  for (int i = 0; i < kP2Items; ++i) rk[i] += start[(d[i] >> w2) & fmask];
+  if (tid < nb2)
+    delta[tid] = win0 + (static_cast<unsigned long long>(tid) << w2) + atomicAdd(cur + tid, hist[tid]) - start[tid];
+  if (tid + kP2Threads < nb2) {  // fan-outs above kP2Threads (16-byte payloads at 2^30)
+    const int i = tid + kP2Threads;
+    delta[i] = win0 + (static_cast<unsigned long long>(i) << w2) + atomicAdd(cur + i, hist[i]) - start[i];
+  }
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < kP2Items; ++i) {
-    sv[rk[i]] = v[i];
-    sd[rk[i]] = d[i];
+    const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
+    sv[s] = v[i];
+    sd[s] = d[i];
   }
-  if (tid < nb2) delta[tid] = win0 + (static_cast<unsigned long long>(tid) << w2) + g - start[tid];
   __syncthreads();
 #pragma unroll 4
   for (int s = tid; s < kP2Tile; s += kP2Threads) {

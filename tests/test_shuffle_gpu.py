@@ -545,3 +545,27 @@ def test_partitioned_512_coarse_buckets(bsg, cuda):
     assert np.array_equal(outs[0][:4096].cpu().numpy().view(np.uint64), O.shuffle_indices_range(m, 30, PHILOX, 24, 0, 4096))
     del vals, outs
     cuda.cuda.empty_cache()
+
+
+def test_partitioned_512_fine_windows_16_byte(bsg, cuda):
+    """C5's per-GPU unit: 2^30 16-byte records take 512 coarse buckets x 512 fine windows (two bins per
+    thread in both scans).  The keys of the output must be the permutation itself (single pass), and the
+    first entries the oracle's."""
+    m = 1 << 30
+    rec = cuda.arange(2 * m, dtype=cuda.int64, device="cuda").view(cuda.complex128)
+    old = bsg.set_path(2)
+    try:
+        out = bsg.shuffle_values(rec, cfg_of(bsg, seed=55))
+    finally:
+        bsg.set_path(old)
+    del rec
+    keys = out.view(cuda.int64).view(m, 2)[:, 0] // 2
+    vals_ok = cuda.equal(out.view(cuda.int64).view(m, 2)[:, 1], out.view(cuda.int64).view(m, 2)[:, 0] + 1)
+    del out
+    cuda.cuda.empty_cache()
+    perm = bsg.shuffle_indices(m, cfg_of(bsg, seed=55), device="cuda")
+    assert vals_ok
+    assert cuda.equal(keys, perm)
+    assert np.array_equal(perm[:4096].cpu().numpy().view(np.uint64), O.shuffle_indices_range(m, 55, PHILOX, 24, 0, 4096))
+    del keys, perm
+    cuda.cuda.empty_cache()
