@@ -285,7 +285,7 @@ def ours_arm(args, rank, world, local):
         pow2 = (m_total & (m_total - 1)) == 0
         if not pow2:
             dominant = "bsg::k_compact_smem"
-        elif world == 1 and m_total * eb >= (256 << 20):
+        elif world == 1 and m_total * eb >= (256 << 20) and eb <= 8:
             dominant = "bsg::k_part1+k_part2+k_place"  # partitioned path (whole domain, >= 256 MiB)
         else:
             dominant = "bsg::k_pow2"  # counter-range shards take the single fused pass
