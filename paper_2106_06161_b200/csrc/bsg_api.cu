@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -81,6 +82,7 @@ struct DeviceCtx {
   DevBuf keys;     // round keys for non-24-round Philox
   DevBuf st_in, st_out, st_idx, st_tmp;  // host-pointer staging / temporaries
   DevBuf part;                           // partitioned-path workspace
+  std::deque<std::vector<uint32_t>> captured_keys;  // host key schedules read by captured graphs
   cudaEvent_t ws_done = nullptr;
   bool ready = false;
 };
@@ -160,11 +162,21 @@ bsg_status build_params(int variant, int bits, uint64_t seed, int rounds, BijPar
 }
 
 // Orders this call after every earlier kernel of the context (any stream).
+// True while `s` is being captured into a CUDA graph.  Captured calls skip the cross-stream workspace
+// ordering (a graph replays on one stream; replays must not overlap other calls on the same device) and every
+// host synchronisation; the workspaces must already be sized by one uncaptured call of the same shape.
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return s != nullptr && cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+
 bsg_status ws_begin(DeviceCtx* c, cudaStream_t s) {
+  if (capturing(s)) return BSG_OK;
   BSG_CUDA(cudaStreamWaitEvent(s, c->ws_done, 0));
   return BSG_OK;
 }
 bsg_status ws_end(DeviceCtx* c, cudaStream_t s) {
+  if (capturing(s)) return BSG_OK;
   BSG_CUDA(cudaEventRecord(c->ws_done, s));
   return BSG_OK;
 }
@@ -174,9 +186,17 @@ bsg_status upload_keys(DeviceCtx* c, BijParams& p, uint64_t seed, cudaStream_t s
   if (p.variant != bsg::kPhilox || p.rounds == 24) return BSG_OK;
   std::vector<uint32_t> k(static_cast<size_t>(p.rounds));
   for (int i = 0; i < p.rounds; ++i) k[i] = bsg::round_key(seed, i);
-  BSG_CUDA(c->keys.ensure(k.size() * 4));
-  BSG_CUDA(cudaMemcpyAsync(c->keys.p, k.data(), k.size() * 4, cudaMemcpyHostToDevice, s));
-  BSG_CUDA(cudaStreamSynchronize(s));  // k is a stack temporary
+  if (capturing(s)) {
+    // the graph's copy node reads this host array at every replay: keep it for the context's lifetime
+    if (c->keys.bytes < k.size() * 4) return fail(BSG_EINVAL, "graph capture: run this call once uncaptured first");
+    c->captured_keys.push_back(std::move(k));
+    const std::vector<uint32_t>& kk = c->captured_keys.back();
+    BSG_CUDA(cudaMemcpyAsync(c->keys.p, kk.data(), kk.size() * 4, cudaMemcpyHostToDevice, s));
+  } else {
+    BSG_CUDA(c->keys.ensure(k.size() * 4));
+    BSG_CUDA(cudaMemcpyAsync(c->keys.p, k.data(), k.size() * 4, cudaMemcpyHostToDevice, s));
+    BSG_CUDA(cudaStreamSynchronize(s));  // k is a stack temporary
+  }
   p.gkeys = static_cast<const uint32_t*>(c->keys.p);
   return BSG_OK;
 }
@@ -184,17 +204,26 @@ bsg_status upload_keys(DeviceCtx* c, BijParams& p, uint64_t seed, cudaStream_t s
 // Prepares the look-back workspace for a compacting launch over `tiles`.
 bsg_status lookback_prepare(DeviceCtx* c, uint64_t tiles, cudaStream_t s, bsg::Lookback& lb) {
   const size_t need = std::max<uint64_t>(tiles, 1) * sizeof(unsigned long long);
+  lb.status = static_cast<unsigned long long*>(c->status.p);
+  lb.tile_counter = static_cast<unsigned int*>(c->scratch.p);
+  if (capturing(s)) {
+    // A replayed graph cannot advance the epoch: it clears its status words and uses epoch 1, which
+    // uncaptured launches never use.
+    if (c->status.bytes < need) return fail(BSG_EINVAL, "graph capture: run this call once uncaptured first");
+    BSG_CUDA(cudaMemsetAsync(c->status.p, 0, need, s));
+    lb.epoch = 1;
+    return BSG_OK;
+  }
   if (c->status.bytes < need) {
     BSG_CUDA(cudaStreamSynchronize(s));
     BSG_CUDA(c->status.ensure(need, true));
-    c->epoch = 0;
-  }
-  if (++c->epoch >= (1u << 22)) {  // epoch wrap: clear stale words once
-    BSG_CUDA(cudaMemsetAsync(c->status.p, 0, c->status.bytes, s));
+    lb.status = static_cast<unsigned long long*>(c->status.p);
     c->epoch = 1;
   }
-  lb.status = static_cast<unsigned long long*>(c->status.p);
-  lb.tile_counter = static_cast<unsigned int*>(c->scratch.p);
+  if (++c->epoch >= (1u << 22) || c->epoch < 2) {  // wrap: clear stale words once (epoch 1 is the graphs')
+    BSG_CUDA(cudaMemsetAsync(c->status.p, 0, c->status.bytes, s));
+    c->epoch = 2;
+  }
   lb.epoch = c->epoch;
   return BSG_OK;
 }
@@ -265,9 +294,9 @@ bsg_status shuffle_device(DeviceCtx* c, const void* in, void* out, uint64_t m, u
   if (m <= 2) {  // shuffle.hpp:228-240 / 249-259: variant and rounds ignored
     const uint64_t bit = (m == 2) ? (bsg::mix64(cfg.seed) & 1) : 0;
     if (idx) {
-      const uint64_t v[2] = {bit, bit ^ 1};
-      BSG_CUDA(cudaMemcpyAsync(out, v, m * 8, cudaMemcpyHostToDevice, s));
-      BSG_CUDA(cudaStreamSynchronize(s));
+      uint64_t* o = static_cast<uint64_t*>(out);
+      BSG_CUDA(bsg::launch_store_u64(reinterpret_cast<unsigned long long*>(o), bit, s));
+      if (m == 2) BSG_CUDA(bsg::launch_store_u64(reinterpret_cast<unsigned long long*>(o + 1), bit ^ 1, s));
     } else {
       for (uint64_t k = 0; k < m; ++k)
         BSG_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + k * ob, static_cast<const char*>(in) + (k ^ bit) * eb, eb,

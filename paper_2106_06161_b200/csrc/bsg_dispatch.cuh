@@ -72,8 +72,8 @@ cudaError_t dispatch_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-template <int KIND, typename T>
-cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
+template <int KIND, typename T, int NT>
+cudaError_t run_batched_nt(const BatchedLaunch& a, cudaStream_t s) {
   const size_t row_bytes = static_cast<size_t>(a.m) * sizeof(T);
   const size_t stride = (row_bytes + 15) / 16 * 16;
   const size_t smem = 2 * stride;  // double-buffered rows
@@ -81,7 +81,7 @@ cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
   const uintptr_t base = reinterpret_cast<uintptr_t>(a.in);
   if (row_bytes % 16 == 0 && base % 16 == 0) mode = 1;
   else if (row_bytes % 4 == 0 && base % 4 == 0) mode = 2;
-  auto kern = k_batched<KIND, T>;
+  auto kern = k_batched<KIND, T, NT>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -89,14 +89,28 @@ cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
   if (per_sm < 1) return cudaErrorNotSupported;
-  const uint64_t want = static_cast<uint64_t>(sms) * per_sm;
-  const unsigned grid = static_cast<unsigned>(a.batch < want ? a.batch : want);
-  kern<<<grid, kThreads, smem, s>>>(static_cast<const T*>(a.in), static_cast<T*>(a.out), a.batch, a.m, a.seed, a.p,
-                                    mode, static_cast<uint32_t>(stride));
+  // Every CTA takes the same number of rows (ceil(batch / resident)), so the last wave has no stragglers.
+  const uint64_t resident = static_cast<uint64_t>(sms) * per_sm;
+  const uint64_t rows_per_cta = (a.batch + resident - 1) / resident;
+  const uint64_t grid = (a.batch + rows_per_cta - 1) / rows_per_cta;
+  kern<<<static_cast<unsigned>(grid), NT, smem, s>>>(static_cast<const T*>(a.in), static_cast<T*>(a.out), a.batch,
+                                                      a.m, a.seed, a.p, mode, static_cast<uint32_t>(stride));
   note_launch();
   return cudaGetLastError();
+}
+
+// Block size by row length: about 16 counters per thread for short rows (C4: 1024 counters -> 64 threads).
+#ifndef BSG_BATCHED_PER_THREAD
+#define BSG_BATCHED_PER_THREAD 16
+#endif
+template <int KIND, typename T>
+cudaError_t run_batched(const BatchedLaunch& a, cudaStream_t s) {
+  const uint64_t n = 1ULL << a.p.bits;
+  if (n <= 64 * BSG_BATCHED_PER_THREAD) return run_batched_nt<KIND, T, 64>(a, s);
+  if (n <= 128 * BSG_BATCHED_PER_THREAD) return run_batched_nt<KIND, T, 128>(a, s);
+  return run_batched_nt<KIND, T, kThreads>(a, s);
 }
 
 template <typename T>

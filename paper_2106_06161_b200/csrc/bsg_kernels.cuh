@@ -539,18 +539,41 @@ __device__ __forceinline__ uint32_t philox_keys_fwd(uint32_t x, const uint32_t* 
   return (s0 << R) | (s1 & RM);
 }
 
+// U counters in lock step (round-major), so the U independent dependency
+// chains interleave instruction by instruction (ptxas keeps a counter-major
+// sequence of unrolled rounds back to back, which stalls on every round).
+template <int D, int NR, int U>
+__device__ __forceinline__ void philox_keys_fwd_x(uint32_t (&x)[U], const uint32_t* k, int L, int R, uint32_t LM,
+                                                  uint32_t RM) {
+  uint32_t s0[U], s1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    s0[u] = x[u] >> R;
+    s1[u] = x[u] & RM;
+  }
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) philox_round<D>(s0[u], s1[u], k[i], L, LM, RM);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) x[u] = (s0[u] << R) | (s1[u] & RM);
+}
+
 // Rows are double-buffered in shared memory: while shuffle b is evaluated, the
 // row of the CTA's next shuffle streams in with cp.async and its round keys
 // are derived by the first `rounds` threads, so neither the load latency nor
-// the key schedule serialises with the cipher.
+// the key schedule serialises with the cipher.  NT threads per row: small
+// blocks give each thread many independent counters (ILP for the 24-round
+// chains, whose keys sit in registers shared by all of them).
 // row_mode: 1 = 16-byte cp.async chunks, 2 = 4-byte chunks, 0 = plain loads.
-template <int KIND, typename T>
-__global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, T* __restrict__ out, uint64_t batch,
+template <int KIND, typename T, int NT>
+__global__ void __launch_bounds__(NT) k_batched(const T* __restrict__ in, T* __restrict__ out, uint64_t batch,
                                                       uint32_t m, uint64_t seed, BijParams p, int row_mode,
                                                       uint32_t row_stride_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_keys[2][kBatchedMaxRounds];
-  __shared__ uint32_t s_wcnt[2][kWarps];
+  __shared__ uint32_t s_wcnt[2][(NT / 32)];
   constexpr bool kFast = (KIND == kKindPh0 || KIND == kKindPh1);
   constexpr int D = (KIND == kKindPh1 || KIND == kKindPh1G) ? 1 : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -564,23 +587,24 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
     const unsigned char* src = reinterpret_cast<const unsigned char*>(in + b * m);
     unsigned char* dst = smem_raw + buf * row_stride_bytes;
     if (row_mode == 1) {
-      for (uint32_t o = tid * 16; o < row_bytes; o += kThreads * 16) {
+      for (uint32_t o = tid * 16; o < row_bytes; o += NT * 16) {
         const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + o));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + o) : "memory");
       }
     } else if (row_mode == 2) {
-      for (uint32_t o = tid * 4; o < row_bytes; o += kThreads * 4) {
+      for (uint32_t o = tid * 4; o < row_bytes; o += NT * 4) {
         const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + o));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + o) : "memory");
       }
     } else {
       T* r = reinterpret_cast<T*>(dst);
-      for (uint32_t i = tid; i < m; i += kThreads) r[i] = in[b * m + i];
+      for (uint32_t i = tid; i < m; i += NT) r[i] = in[b * m + i];
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   auto make_keys = [&](uint64_t b, int buf) {
-    if (KIND != kKindLcg && tid < p.rounds) s_keys[buf][tid] = round_key(seed + b, tid);
+    if (KIND != kKindLcg)
+      for (int i = tid; i < p.rounds; i += NT) s_keys[buf][i] = round_key(seed + b, i);
   };
 
   int buf = 0;
@@ -621,12 +645,29 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
       else return philox_keys_fwd<D, 0>(c, keys, p.L, p.R, p.LM, p.RM, p.rounds);
     };
     if (pow2) {
-#pragma unroll 4
-      for (uint32_t c = tid; c < n; c += kThreads) st_out<T>(row_out + c, s_row[f(c)]);
+      // BSG_BATCHED_ILP independent counters per thread in flight
+#ifndef BSG_BATCHED_ILP
+#define BSG_BATCHED_ILP 8
+#endif
+      constexpr int U = BSG_BATCHED_ILP;
+      for (uint32_t c0 = tid; c0 < n; c0 += NT * U) {
+        uint32_t y[U];  // counters past n are evaluated, never stored
+        if constexpr (kRegKeys) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) y[u] = c0 + u * NT;
+          philox_keys_fwd_x<D, 24, U>(y, kr, p.L, p.R, p.LM, p.RM);
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) y[u] = f(c0 + u * NT);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * NT < n) st_out<T>(row_out + c0 + u * NT, s_row[y[u]]);
+      }
     } else {
       uint32_t base = 0;
       int cb = 0;
-      for (uint32_t c0 = 0; c0 < n; c0 += kThreads) {
+      for (uint32_t c0 = 0; c0 < n; c0 += NT) {
         const uint32_t c = c0 + tid;
         const uint32_t y = f(c);
         const bool keep = (c < n) && (y < m);
@@ -635,7 +676,7 @@ __global__ void __launch_bounds__(kThreads) k_batched(const T* __restrict__ in, 
         __syncthreads();
         uint32_t before = 0, total = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
+        for (int w = 0; w < (NT / 32); ++w) {
           const uint32_t x = s_wcnt[cb][w];
           before += (w < warp) ? x : 0;
           total += x;

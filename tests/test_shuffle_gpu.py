@@ -569,3 +569,46 @@ def test_partitioned_512_fine_windows_16_byte(bsg, cuda):
     assert np.array_equal(perm[:4096].cpu().numpy().view(np.uint64), O.shuffle_indices_range(m, 55, PHILOX, 24, 0, 4096))
     del keys, perm
     cuda.cuda.empty_cache()
+
+
+def test_cuda_graph_capture_and_replay(bsg, cuda):
+    """Device-pointer calls are capturable into a CUDA graph (after one uncaptured call sizes the workspaces);
+    every replay recomputes the shuffle of the input's current contents -- including the look-back path,
+    whose status words a replay cannot re-epoch, and generic round counts, whose keys a replay re-uploads."""
+    cases = [((1 << 20), 24, cuda.int64, "pow2"), ((1 << 20) + 7, 24, cuda.int64, "lookback"),
+             ((1 << 16) + 1, 9, cuda.int32, "generic rounds"), ((1 << 25), 24, cuda.int64, "partitioned")]
+    for m, rounds, dt, what in cases:
+        cfg = cfg_of(bsg, seed=77, rounds=rounds)
+        vals = cuda.arange(m, dtype=dt, device="cuda")
+        out = cuda.empty_like(vals)
+        old = bsg.set_path(2 if what == "partitioned" else 0)
+        try:
+            bsg.shuffle_values_into(vals, cfg, out)  # sizes the workspaces outside the capture
+            s = cuda.cuda.Stream()
+            g = cuda.cuda.CUDAGraph()
+            with cuda.cuda.stream(s):
+                cuda.cuda.synchronize()
+                with cuda.cuda.graph(g, stream=s):
+                    bsg.shuffle_values_into(vals, cfg, out)
+            for k in range(3):
+                vals.copy_(cuda.arange(m, dtype=dt, device="cuda") * (k + 2) + k)
+                out.zero_()
+                g.replay()
+                cuda.cuda.synchronize()
+                exp = bsg.shuffle_values(vals, cfg)
+                assert cuda.equal(out, exp), (what, k)
+        finally:
+            bsg.set_path(old)
+    rows = cuda.arange(1024, dtype=cuda.int32, device="cuda").repeat(64, 1)
+    outb = cuda.empty_like(rows)
+    bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=5), out=outb)
+    g = cuda.cuda.CUDAGraph()
+    s = cuda.cuda.Stream()
+    with cuda.cuda.stream(s):
+        cuda.cuda.synchronize()
+        with cuda.cuda.graph(g, stream=s):
+            bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=5), out=outb)
+    outb.zero_()
+    g.replay()
+    cuda.cuda.synchronize()
+    assert cuda.equal(outb, bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=5)))
