@@ -626,10 +626,7 @@ __global__ void __launch_bounds__(NT) k_batched(const T* __restrict__ in, T* __r
     const uint32_t* keys = s_keys[buf];
     T* row_out = out + b * m;
     const uint64_t sb = seed + b;
-#ifndef BSG_BATCHED_SMEM_KEYS
-#define BSG_BATCHED_SMEM_KEYS 0
-#endif
-    constexpr bool kRegKeys = kFast && !BSG_BATCHED_SMEM_KEYS;
+    constexpr bool kRegKeys = kFast;  // 24 keys held in registers, shared by all of the thread's counters
     uint32_t kr[kRegKeys ? 24 : 1];
     if constexpr (kRegKeys) {
 #pragma unroll
@@ -641,7 +638,6 @@ __global__ void __launch_bounds__(NT) k_batched(const T* __restrict__ in, T* __r
     auto f = [&](uint32_t c) -> uint32_t {
       if constexpr (KIND == kKindLcg) return (la * c + lc) & mask32;
       else if constexpr (kRegKeys) return philox_keys_fwd<D, 24>(c, kr, p.L, p.R, p.LM, p.RM, 24);
-      else if constexpr (kFast) return philox_keys_fwd<D, 24>(c, keys, p.L, p.R, p.LM, p.RM, 24);
       else return philox_keys_fwd<D, 0>(c, keys, p.L, p.R, p.LM, p.RM, p.rounds);
     };
     if (pow2) {
