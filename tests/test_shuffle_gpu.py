@@ -612,3 +612,26 @@ def test_cuda_graph_capture_and_replay(bsg, cuda):
     g.replay()
     cuda.cuda.synchronize()
     assert cuda.equal(outb, bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=5)))
+
+
+def test_partitioned_full_32_bit_domain(bsg, cuda):
+    """The largest partitioned shape: 2^32 u32 (bits = 32, 512 x 512 fan-out, write-back positions that use all
+    32 bits of the position tables).  Equal to the single pass; head and tail against the oracle."""
+    m = 1 << 32
+    vals = cuda.arange(m, dtype=cuda.int64, device="cuda").to(cuda.int32)  # low 32 bits of the index
+    outs = []
+    for path in (2, 1):
+        old = bsg.set_path(path)
+        try:
+            outs.append(bsg.shuffle_values(vals, cfg_of(bsg, seed=32)))
+        finally:
+            bsg.set_path(old)
+    del vals
+    cuda.cuda.empty_cache()
+    assert cuda.equal(outs[0], outs[1])
+    head = outs[0][:2048].cpu().numpy().view(np.uint32).astype(np.uint64)
+    tail = outs[0][-2048:].cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.array_equal(head, O.shuffle_indices_range(m, 32, PHILOX, 24, 0, 2048))
+    assert np.array_equal(tail, O.shuffle_indices_range(m, 32, PHILOX, 24, m - 2048, m))
+    del outs
+    cuda.cuda.empty_cache()
