@@ -102,6 +102,36 @@ __device__ __forceinline__ void scan_bins(const uint32_t* hist, uint32_t* start,
   __syncthreads();  // start[] is read by other threads right after (two bins per thread when nb > blockDim)
 }
 
+// mbarrier + bulk-copy helpers (TMA-fed kernels below).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+
 // P1: stream the input, route by coarse destination bucket.
 template <int KIND, int D, typename T>
 __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) k_part1(const T* __restrict__ in, T* __restrict__ tv,
@@ -168,6 +198,84 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) 
   }
 }
 
+// P1, persistent and TMA-fed: the values of the next tile stream into a
+// staging buffer (one bulk copy, mbarrier completion) while the current tile's
+// destinations are computed, so the scatter reads them from shared memory
+// instead of issuing the DRAM loads after the scan.
+template <int KIND, int D, typename T>
+__global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in, T* __restrict__ tv,
+                                                       uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
+                                                       BijParams p, int bshift, int nb, uint64_t w1,
+                                                       const uint32_t* __restrict__ dsrc, uint32_t ntiles) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* gv = reinterpret_cast<T*>(smem);                    // staging: values of the tile in flight
+  T* sv = gv + kP1Tile;                                  // sorted values
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);  // sorted destinations
+  __shared__ uint32_t hist[kMaxB1], start[kMaxB1], wt[32];
+  __shared__ uint32_t delta[kMaxB1];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
+  __syncthreads();
+  auto issue = [&](uint32_t t) {
+    mbar_expect_tx(&bar, kP1Tile * sizeof(T));
+    bulk_g2s(gv, in + static_cast<uint64_t>(t) * kP1Tile, kP1Tile * sizeof(T), &bar);
+  };
+  if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
+  uint32_t phase = 0;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
+    const uint32_t base = t * kP1Tile + tid;
+    uint32_t dst[kP1Items], rk[kP1Items];
+#pragma unroll
+    for (int i = 0; i < kP1Items; ++i) {
+      if constexpr (KIND == kKindDestArray) dst[i] = __ldcs(dsrc + base + i * kP1Threads);
+      else dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
+      rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
+    }
+    __syncthreads();
+    scan_bins(hist, start, nb, wt);
+    uint32_t g[2] = {0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = tid + k * kP1Threads;
+      if (i < nb) g[k] = atomicAdd(cur1 + i, hist[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
+    mbar_wait(&bar, phase);  // this tile's values have landed
+#pragma unroll
+    for (int i = 0; i < kP1Items; ++i) {
+      sv[rk[i]] = gv[tid + i * kP1Threads];
+      sd[rk[i]] = dst[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = tid + k * kP1Threads;
+      if (i < nb) {
+        delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
+        hist[i] = 0;                                                  // next tile
+      }
+    }
+    __syncthreads();  // staging consumed; sorted tile and delta complete
+    if (tid == 0 && t + gridDim.x < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(t + gridDim.x);
+    }
+#pragma unroll 4
+    for (int s = tid; s < kP1Tile; s += kP1Threads) {
+      const uint32_t d = sd[s];
+      const uint32_t pos = delta[d >> bshift] + s;
+      __stcs(tv + pos, sv[s]);
+      __stcs(td + pos, d);
+    }
+    __syncthreads();  // sorted buffers, delta and start reused by the next tile
+  }
+}
+
 // P2: split each coarse bucket into fine windows of 2^w2 elements (one tile per CTA; used for 16-byte records,
 // whose staging would not fit twice next to the sorted tile -- k_part2t below is the default).
 template <typename T>
@@ -228,35 +336,6 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) <= 8 ? 3 : 2)
 // destinations stream into a staging buffer with two bulk copies
 // (cp.async.bulk, completion on an mbarrier), so the DRAM latency of the
 // loads leaves the per-tile critical path.
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
-               "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(done)
-        : "r"(a), "r"(phase)
-        : "memory");
-  }
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                        T* __restrict__ ov, uint16_t* __restrict__ od,
@@ -407,8 +486,26 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   cudaFuncSetAttribute(k_part2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
   cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
   T* tv = static_cast<T*>(a.tmp_values);
-  k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
-      static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in);
+  // Cheap destinations (LCG, a given permutation) leave P1 bound by its loads: the TMA-fed persistent P1 (2 CTAs
+  // per SM) hides them (C2 LCG 7.69 -> 7.07 ms).  The 24-round Philox needs the third CTA per SM of k_part1 to
+  // keep the integer pipes busy (k_part1t: 5.16 vs 3.97 ms).
+  constexpr bool kTmaP1 = (KIND == kKindLcg || KIND == kKindDestArray) && sizeof(T) <= 8;
+  if (kTmaP1) {
+    const size_t smt = kP1Tile * (2 * sizeof(T) + 4);
+    cudaFuncSetAttribute(k_part1t<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part1t<KIND, D, T>, kP1Threads, smt);
+    const uint64_t tiles = n / kP1Tile;
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
+    k_part1t<KIND, D, T><<<static_cast<unsigned>(grid), kP1Threads, smt, s>>>(
+        static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in,
+        static_cast<uint32_t>(tiles));
+  } else {
+    k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
+        static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in);
+  }
   if constexpr (sizeof(T) <= 8) {  // TMA-fed persistent P2 (2.65 -> 2.45 ms for C2); 16-byte records keep k_part2
     const size_t smt = 2 * kP2Tile * (sizeof(T) + 4);
     cudaFuncSetAttribute(k_part2t<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
