@@ -17,7 +17,9 @@
 //       write the window back coalesced (in place: each CTA reads its whole
 //       range before writing).
 // Every DRAM access is a coalesced run; traffic is ~60 B/element instead of
-// one random 64-B access per 8-B element.  Exact sizes (pow2: each bucket
+// one random 64-B access per 8-B element.  P2 (and P1 for cheap bijections)
+// run persistent with TMA bulk copies of the next tile in flight.  P1 for the
+// 24-round Philox is bound by the integer pipes (the cipher).  Exact sizes (pow2: each bucket
 // receives exactly its window) make the layout static; atomic cursors only
 // order elements inside a bucket, which the final exact placement makes
 // irrelevant -- the output is bit-identical to the single-pass kernel.
@@ -32,6 +34,7 @@ namespace bsg {
 
 namespace {
 
+// Tuning knobs (compile-time; defaults are the measured best, profiles/r01_microbench.md).
 #ifndef BSG_P1_THREADS
 #define BSG_P1_THREADS 256
 #endif
