@@ -245,24 +245,22 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
   BSG_TRY(ws_begin(c, s));
   BSG_TRY(upload_keys(c, p, cfg.seed, s));
   const bool pow2 = (m == (1ULL << bits));
-  if (pow2 && !g_force_compact && g_path != 1 && elem_code > 0 && src.nshards == 0 && c0 == 0 &&
-      c1 == (1ULL << bits) && bsg::partition_eligible(elem_code, bits) &&
+  // Partitioned path: whole power-of-two domains, and whole non-power-of-two domains with elements <= 8 B
+  // (routed by counter, compacted by counter rank in the last pass).
+  if (!g_force_compact && g_path != 1 && elem_code > 0 && src.nshards == 0 && c0 == 0 && c1 == (1ULL << bits) &&
+      (pow2 || elem_code <= 8) && bsg::partition_eligible(elem_code, bits) &&
       auto_partition(m, static_cast<uint64_t>(elem_code))) {
-    const size_t need = bsg::partition_workspace_bytes(elem_code, bits);
+    const size_t need = bsg::partition_workspace_bytes(elem_code, bits, !pow2);
     cudaError_t ae = c->part.ensure(need);
     if (ae == cudaSuccess) {
-      const uint64_t n = 1ULL << bits;
-      char* w = static_cast<char*>(c->part.p);
       bsg::PartitionLaunch P;
+      bsg::partition_layout(elem_code, bits, !pow2, c->part.p, P);
       P.in = src.base;
       P.out = out;
-      P.tmp_values = w;
-      P.tmp_dest = reinterpret_cast<uint32_t*>(w + n * elem_code);
-      P.tmp_dlow = reinterpret_cast<uint16_t*>(w + n * elem_code + n * 4);
-      P.cursors = reinterpret_cast<uint32_t*>(w + n * elem_code + n * 6);
+      P.m = m;
       P.p = p;
       BSG_CUDA(bsg::launch_partition(elem_code, P, s));
-      if (count_dev) BSG_CUDA(bsg::launch_store_u64(count_dev, n, s));
+      if (count_dev) BSG_CUDA(bsg::launch_store_u64(count_dev, m, s));
       return ws_end(c, s);
     }
     cudaGetLastError();  // workspace did not fit: the single-pass kernel needs none
@@ -739,14 +737,10 @@ bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uin
     if (pow2 && g_path != 1 && bsg::partition_eligible(code, bits) &&
         (g_path == 2 || n * static_cast<uint64_t>(elem_bytes) >= g_partition_min_bytes) &&
         c->part.ensure(bsg::partition_workspace_bytes(code, bits)) == cudaSuccess) {
-      char* w = static_cast<char*>(c->part.p);
       bsg::PartitionLaunch P;
+      bsg::partition_layout(code, bits, false, c->part.p, P);
       P.in = values;
       P.out = out;
-      P.tmp_values = w;
-      P.tmp_dest = reinterpret_cast<uint32_t*>(w + n * elem_bytes);
-      P.tmp_dlow = reinterpret_cast<uint16_t*>(w + n * elem_bytes + n * 4);
-      P.cursors = reinterpret_cast<uint32_t*>(w + n * elem_bytes + n * 6);
       P.dest_in = dest;
       P.p.bits = bits;
       BSG_CUDA(bsg::launch_partition(code, P, s));

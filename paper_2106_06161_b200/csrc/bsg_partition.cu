@@ -136,11 +136,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // P1: stream the input, route by coarse destination bucket.
-template <int KIND, int D, typename T>
-__global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) k_part1(const T* __restrict__ in, T* __restrict__ tv,
-                                                         uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
-                                                         BijParams p, int bshift, int nb, uint64_t w1,
-                                                         const uint32_t* __restrict__ dsrc) {
+// PAD: non-power-of-two domain, only inputs j < mv exist (the last tile may be partial); tile0 offsets the
+// tiles of a launch (the partial tail after k_part1t's full tiles).
+template <int KIND, int D, typename T, bool PAD = false>
+__global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2)
+    k_part1(const T* __restrict__ in, T* __restrict__ tv, uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
+            BijParams p, int bshift, int nb, uint64_t w1, const uint32_t* __restrict__ dsrc, uint64_t mv = 0,
+            uint32_t tile0 = 0) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* sv = reinterpret_cast<T*>(smem);
   uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);
@@ -149,7 +151,9 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) 
   const int tid = threadIdx.x;
   for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
   __syncthreads();
-  const uint32_t base = blockIdx.x * kP1Tile + tid;
+  const uint32_t base = (tile0 + blockIdx.x) * kP1Tile + tid;
+  const uint64_t left = PAD ? mv - static_cast<uint64_t>(tile0 + blockIdx.x) * kP1Tile : kP1Tile;
+  const uint32_t nvalid = left < kP1Tile ? static_cast<uint32_t>(left) : static_cast<uint32_t>(kP1Tile);
 #ifndef BSG_P1_LATE_LOAD
 #define BSG_P1_LATE_LOAD 1
 #endif
@@ -157,16 +161,18 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) 
   // loaded straight into their sorted slots after the scan; 0 loads them first so their latency hides under the
   // cipher (103 registers, 2 CTAs/SM; measured 1.5% slower for C2).
   T v[BSG_P1_LATE_LOAD ? 1 : kP1Items];
+  auto valid = [&](int i) { return !PAD || tid + i * kP1Threads < static_cast<int>(nvalid); };
   if constexpr (!BSG_P1_LATE_LOAD) {
 #pragma unroll
-    for (int i = 0; i < kP1Items; ++i) v[i] = __ldcs(in + base + i * kP1Threads);
+    for (int i = 0; i < kP1Items; ++i)
+      if (valid(i)) v[i] = __ldcs(in + base + i * kP1Threads);
   }
   uint32_t dst[kP1Items], rk[kP1Items];
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
     if constexpr (KIND == kKindDestArray) dst[i] = __ldcs(dsrc + base + i * kP1Threads);
     else dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
-    rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
+    if (valid(i)) rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
   }
   __syncthreads();
   scan_bins(hist, start, nb, wt);
@@ -181,6 +187,7 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) 
   for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
+    if (!valid(i)) continue;
     if constexpr (BSG_P1_LATE_LOAD) sv[rk[i]] = __ldcs(in + base + i * kP1Threads);
     else sv[rk[i]] = v[i];
     sd[rk[i]] = dst[i];
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2) 
   }
   __syncthreads();
 #pragma unroll 4
-  for (int s = tid; s < kP1Tile; s += kP1Threads) {
+  for (int s = tid; s < static_cast<int>(nvalid); s += kP1Threads) {
     const uint32_t d = sd[s];
     const uint32_t pos = delta[d >> bshift] + s;
     __stcs(tv + pos, sv[s]);
@@ -339,11 +346,13 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) <= 8 ? 3 : 2)
 // destinations stream into a staging buffer with two bulk copies
 // (cp.async.bulk, completion on an mbarrier), so the DRAM latency of the
 // loads leaves the per-tile critical path.
+// cnt1 != nullptr (non-power-of-two domains): coarse bucket b holds cnt1[b] <= w1 elements, so tile k of the
+// bucket is partial or empty; empty tiles are skipped before their loads are issued.
 template <typename T>
 __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                        T* __restrict__ ov, uint16_t* __restrict__ od,
                                                        uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
-                                                       uint32_t ntiles) {
+                                                       uint32_t ntiles, const uint32_t* __restrict__ cnt1) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* gv = reinterpret_cast<T*>(smem);                    // staging: values of the next tile
   uint32_t* gd = reinterpret_cast<uint32_t*>(gv + kP2Tile);  // staging: destinations
@@ -367,10 +376,22 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     bulk_g2s(gv, tv + e0, kP2Tile * sizeof(T), &bar);
     bulk_g2s(gd, td + e0, kP2Tile * 4, &bar);
   };
+  const uint32_t tpb = static_cast<uint32_t>(w1 / kP2Tile);  // tile slots per coarse bucket
+  auto fill = [&](uint32_t t) -> uint32_t {                   // valid elements of tile t (0: empty)
+    if (!cnt1) return kP2Tile;
+    const uint32_t c = cnt1[t / tpb], k0 = (t % tpb) * kP2Tile;
+    return c > k0 ? min(c - k0, static_cast<uint32_t>(kP2Tile)) : 0u;
+  };
+  auto next = [&](uint32_t t) {
+    while (t < ntiles && fill(t) == 0) t += gridDim.x;
+    return t;
+  };
   uint32_t phase = 0;
-  if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
+  uint32_t t = next(blockIdx.x);
+  if (tid == 0 && t < ntiles) issue(t);
+  for (; t < ntiles; phase ^= 1) {
     mbar_wait(&bar, phase);
+    const uint32_t nv = fill(t), tn = next(t + gridDim.x);
     const uint64_t t0 = static_cast<uint64_t>(t) * kP2Tile;
     const uint64_t coarse = t0 / w1;
     uint32_t d[kP2Items], rk[kP2Items];
@@ -387,13 +408,14 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     }
     if constexpr (BSG_P2T_EARLY) {
       __syncthreads();
-      if (tid == 0 && t + gridDim.x < ntiles) {
+      if (tid == 0 && tn < ntiles) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of staging before the refill
-        issue(t + gridDim.x);
+        issue(tn);
       }
     }
 #pragma unroll
-    for (int i = 0; i < kP2Items; ++i) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
+    for (int i = 0; i < kP2Items; ++i)
+      if (tid + i * kP2Threads < static_cast<int>(nv)) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
     __syncthreads();
     scan_bins(hist, start, nb2, wt);
     uint32_t* cur = cur2 + coarse * nb2;
@@ -407,6 +429,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     }
 #pragma unroll
     for (int i = 0; i < kP2Items; ++i) {
+      if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
       const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
       if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
       else sv[s] = gv[tid + i * kP2Threads];
@@ -415,18 +438,19 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     __syncthreads();  // staging consumed, sorted tile complete, delta ready
     if (tid < nb2) hist[tid] = 0;
     if (tid + kP2Threads < nb2) hist[tid + kP2Threads] = 0;
-    if (!BSG_P2T_EARLY && tid == 0 && t + gridDim.x < ntiles) {
+    if (!BSG_P2T_EARLY && tid == 0 && tn < ntiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of staging before the refill
-      issue(t + gridDim.x);
+      issue(tn);
     }
 #pragma unroll 4
-    for (int s = tid; s < kP2Tile; s += kP2Threads) {
+    for (int s = tid; s < static_cast<int>(nv); s += kP2Threads) {
       const uint32_t dd = sd[s];
       const uint32_t pos = delta[(dd >> w2) & fmask] + s;
       ov[pos] = sv[s];
       od[pos] = static_cast<uint16_t>(dd & wmask);
     }
     __syncthreads();  // sorted buffers and delta reused by the next tile
+    t = tn;
   }
 }
 
@@ -458,6 +482,111 @@ __global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint1
   for (uint32_t i = threadIdx.x; i < W; i += kP3Threads) __stcs(o + i, win[i]);
 }
 
+// Non-power-of-two P3: window w covers counters [w * 2^w2, (w+1) * 2^w2) and holds
+// cnt[w] <= 2^w2 elements (the inputs j < m whose counter f^-1(j) falls in it).
+// Output positions are counter ranks among the survivors: pre[w] (exclusive
+// prefix of the window counts) plus the rank of the counter inside the window,
+// i.e. the window is placed by counter offset in shared memory with one flag
+// byte per slot, each warp ballots its slots in counter order and writes the
+// survivors as contiguous runs -- the same order chained_compact produces
+// (shuffle.hpp:91-147).
+template <typename T>
+__global__ void __launch_bounds__(kP3Threads) k_place_compact(const T* __restrict__ tv2,
+                                                              const uint16_t* __restrict__ od,
+                                                              const uint32_t* __restrict__ cnt,
+                                                              const uint32_t* __restrict__ pre, int w2,
+                                                              T* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t W = 1u << w2, w = blockIdx.x, tid = threadIdx.x;  // W * sizeof(T) == 64 KiB
+  T* win = reinterpret_cast<T*>(smem);
+  uint8_t* occ = smem + W * sizeof(T);  // one flag byte per slot: plain stores, no atomics
+  __shared__ uint32_t wt[kP3Threads / 32];
+  const uint32_t c = cnt[w];
+  for (uint32_t i = tid; i < W / 16; i += kP3Threads) reinterpret_cast<uint4*>(occ)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const T* src = tv2 + (static_cast<uint64_t>(w) << w2);
+  const uint16_t* dd = od + (static_cast<uint64_t>(w) << w2);
+  constexpr int kU = 8;
+  for (uint32_t i0 = tid; i0 < c; i0 += kP3Threads * kU) {
+    T v[kU];
+    uint32_t slot[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * kP3Threads;
+      if (i < c) {
+        slot[u] = __ldcs(reinterpret_cast<const unsigned short*>(dd) + i);
+        v[u] = __ldcs(src + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * kP3Threads < c) {
+        win[slot[u]] = v[u];
+        occ[slot[u]] = 1;
+      }
+  }
+  __syncthreads();
+  // Warp q owns slots [q * 32 * kPer, (q + 1) * 32 * kPer), read lane-interleaved (conflict-free): chunk k of the
+  // warp is slots base + 32k + lane, so (warp, chunk, lane) order is counter order.
+  constexpr int kPer = (65536 / static_cast<int>(sizeof(T))) / kP3Threads;  // 16 for u64, 32 for u32
+  const uint32_t lane = tid & 31, warp = tid >> 5, wbase = warp * 32 * kPer;
+  const uint32_t lt = (1u << lane) - 1u;
+  T v[kPer];
+  uint32_t mk[kPer], nk = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t slot = wbase + 32 * k + lane;
+    const bool f = occ[slot] != 0;
+    if (f) v[k] = win[slot];
+    mk[k] = __ballot_sync(0xFFFFFFFFu, f);
+    nk += __popc(mk[k]);
+  }
+  if (lane == 0) wt[warp] = nk;
+  __syncthreads();
+  // survivors of chunk k go out as one contiguous run (counter order), straight from registers
+  uint32_t pos = pre[w];
+  for (uint32_t q = 0; q < warp; ++q) pos += wt[q];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if ((mk[k] >> lane) & 1u) __stcs(out + pos + __popc(mk[k] & lt), v[k]);
+    pos += __popc(mk[k]);
+  }
+}
+
+// Exclusive prefix of n u32 counts (one CTA; n <= 2^20 windows).
+__global__ void __launch_bounds__(1024) k_window_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pre,
+                                                     uint32_t n) {
+  __shared__ uint32_t wt[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (n + 1023) / 1024, b = tid * per;
+  uint32_t sum = 0;
+  for (uint32_t k = 0; k < per && b + k < n; ++k) sum += cnt[b + k];
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= static_cast<uint32_t>(o)) x += y;
+  }
+  if (lane == 31) wt[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = wt[lane];
+    uint32_t z = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, o);
+      if (lane >= static_cast<uint32_t>(o)) z += y;
+    }
+    wt[lane] = z - v;
+  }
+  __syncthreads();
+  uint32_t run = wt[warp] + x - sum;
+  for (uint32_t k = 0; k < per && b + k < n; ++k) {
+    pre[b + k] = run;
+    run += cnt[b + k];
+  }
+}
+
 template <typename T>
 int window_log2() {
   return sizeof(T) == 4 ? 14 : (sizeof(T) == 8 ? 13 : 12);  // 64 KiB smem window
@@ -477,6 +606,9 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   int s1, s2;
   part_split(b, w2, s1, s2);
   const uint64_t n = 1ULL << b, w1 = 1ULL << (b - s1);
+  const uint64_t m = a.m ? a.m : n;  // inputs; m < n: non-power-of-two domain (only for elements <= 8 B)
+  const bool pad = m < n;
+  if (pad && sizeof(T) > 8) return cudaErrorNotSupported;
   const int nb1 = 1 << s1, nb2 = 1 << s2;
   uint32_t* cur1 = a.cursors;
   uint32_t* cur2 = a.cursors + nb1;
@@ -485,42 +617,63 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   const size_t sm1 = kP1Tile * (sizeof(T) + 4);
   const size_t sm2 = kP2Tile * (sizeof(T) + 4);
   const size_t sm3 = (size_t{1} << w2) * sizeof(T);
-  cudaFuncSetAttribute(k_part1<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
+  cudaFuncSetAttribute(k_part1<KIND, D, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
+  cudaFuncSetAttribute(k_part1<KIND, D, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
   cudaFuncSetAttribute(k_part2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2));
   cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   T* tv = static_cast<T*>(a.tmp_values);
+  const uint64_t tiles1 = (m + kP1Tile - 1) / kP1Tile, full1 = m / kP1Tile;
   // Cheap destinations (LCG, a given permutation) leave P1 bound by its loads: the TMA-fed persistent P1 (2 CTAs
   // per SM) hides them (C2 LCG 7.69 -> 7.07 ms).  The 24-round Philox needs the third CTA per SM of k_part1 to
   // keep the integer pipes busy (k_part1t: 5.16 vs 3.97 ms).
   constexpr bool kTmaP1 = (KIND == kKindLcg || KIND == kKindDestArray) && sizeof(T) <= 8;
-  if (kTmaP1) {
+  uint64_t done1 = 0;
+  if (kTmaP1 && full1 > 0) {
     const size_t smt = kP1Tile * (2 * sizeof(T) + 4);
     cudaFuncSetAttribute(k_part1t<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part1t<KIND, D, T>, kP1Threads, smt);
-    const uint64_t tiles = n / kP1Tile;
-    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
+    const uint64_t grid = std::min<uint64_t>(full1, static_cast<uint64_t>(sms) * std::max(per, 1));
     k_part1t<KIND, D, T><<<static_cast<unsigned>(grid), kP1Threads, smt, s>>>(
         static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in,
-        static_cast<uint32_t>(tiles));
-  } else {
-    k_part1<KIND, D, T><<<static_cast<unsigned>(n / kP1Tile), kP1Threads, sm1, s>>>(
-        static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in);
+        static_cast<uint32_t>(full1));
+    done1 = full1;
   }
+  if (done1 < tiles1) {
+    if (pad)
+      k_part1<KIND, D, T, true><<<static_cast<unsigned>(tiles1 - done1), kP1Threads, sm1, s>>>(
+          static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, m,
+          static_cast<uint32_t>(done1));
+    else
+      k_part1<KIND, D, T, false><<<static_cast<unsigned>(tiles1 - done1), kP1Threads, sm1, s>>>(
+          static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, m,
+          static_cast<uint32_t>(done1));
+  }
+  // P2 writes the fine windows into `out` itself (power of two: exact sizes) or into a counter-sized buffer.
+  T* p2out = pad ? static_cast<T*>(a.tmp_values2) : static_cast<T*>(a.out);
   if constexpr (sizeof(T) <= 8) {  // TMA-fed persistent P2 (2.65 -> 2.45 ms for C2); 16-byte records keep k_part2
     const size_t smt = 2 * kP2Tile * (sizeof(T) + 4);
     cudaFuncSetAttribute(k_part2t<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T>, kP2Threads, smt);
-    const uint64_t tiles = n / kP2Tile;
+    const uint64_t tiles = n / kP2Tile;  // tile slots; in a padded domain the tail of every bucket is empty
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
-    k_part2t<T><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
-                                                                       a.tmp_dlow, cur2, w2, nb2, w1,
-                                                                       static_cast<uint32_t>(tiles));
+    k_part2t<T><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(tv, a.tmp_dest, p2out, a.tmp_dlow, cur2, w2, nb2,
+                                                                       w1, static_cast<uint32_t>(tiles),
+                                                                       pad ? cur1 : nullptr);
+    if (pad) {
+      const uint32_t nwin = static_cast<uint32_t>(n >> w2);
+      k_window_scan<<<1, 1024, 0, s>>>(cur2, a.win_prefix, nwin);
+      const size_t smc = sm3 + (size_t{1} << w2);  // window + one flag byte per counter
+      cudaFuncSetAttribute(k_place_compact<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smc));
+      k_place_compact<T><<<nwin, kP3Threads, smc, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, w2,
+                                                        static_cast<T*>(a.out));
+      note_launch(5);
+      return cudaGetLastError();
+    }
   } else {
     k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
                                                                             a.tmp_dlow, cur2, w2, nb2, w1);
@@ -716,9 +869,29 @@ bool partition_eligible(int elem_code, int bits) {
          (bits - s1) >= kP2TileLog && bits >= 14;
 }
 
-size_t partition_workspace_bytes(int elem_code, int bits) {
+void partition_layout(int elem_code, int bits, bool pad, void* workspace, PartitionLaunch& P) {
   const uint64_t n = 1ULL << bits;
-  return n * static_cast<uint64_t>(elem_code) + n * 4 + n * 2 + kCursorWords * 4 + 3 * 256;
+  char* w = static_cast<char*>(workspace);
+  P.tmp_values = w;
+  w += n * static_cast<uint64_t>(elem_code);
+  P.tmp_dest = reinterpret_cast<uint32_t*>(w);
+  w += n * 4;
+  P.tmp_dlow = reinterpret_cast<uint16_t*>(w);
+  w += n * 2;
+  P.cursors = reinterpret_cast<uint32_t*>(w);
+  w += (kCursorWords * 4 + 255) / 256 * 256;
+  if (pad) {
+    P.win_prefix = reinterpret_cast<uint32_t*>(w);
+    w += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 255) / 256 * 256;
+    P.tmp_values2 = w;
+  }
+}
+
+size_t partition_workspace_bytes(int elem_code, int bits, bool pad) {
+  const uint64_t n = 1ULL << bits;
+  size_t b = n * static_cast<uint64_t>(elem_code) + n * 4 + n * 2 + (kCursorWords * 4 + 255) / 256 * 256;
+  if (pad) b += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 255) / 256 * 256 + n * static_cast<uint64_t>(elem_code);
+  return b;
 }
 
 cudaError_t launch_partition(int elem_code, const PartitionLaunch& a, cudaStream_t s) {

@@ -15,6 +15,12 @@ struct PartitionLaunch {
   uint32_t* cursors = nullptr;   // bucket append cursors
   const uint32_t* dest_in = nullptr;  // given destinations (scatter by permutation) instead of f^-1
   BijParams p;
+  // Non-power-of-two domains (m < 2^bits, elements <= 8 B): the m inputs are routed by their counter
+  // f^-1(j), P2 fills counter-sized windows in tmp_values2, and the last pass compacts each window by counter
+  // rank using the window-count prefix in win_prefix.  m == 0 means m == 2^bits.
+  uint64_t m = 0;
+  void* tmp_values2 = nullptr;     // n * elem bytes
+  uint32_t* win_prefix = nullptr;  // n >> window_log2 words
 };
 
 struct RouteLaunch {
@@ -36,7 +42,9 @@ cudaError_t launch_route(int elem_code, const RouteLaunch& a, cudaStream_t s);
 cudaError_t launch_exclusive_prefix_u64(const unsigned long long* c, unsigned long long* o, int n, cudaStream_t s);
 
 bool partition_eligible(int elem_code, int bits);
-size_t partition_workspace_bytes(int elem_code, int bits);
+size_t partition_workspace_bytes(int elem_code, int bits, bool pad = false);
+// Carves the workspace into the launch's temporaries (same layout as partition_workspace_bytes).
+void partition_layout(int elem_code, int bits, bool pad, void* workspace, PartitionLaunch& P);
 cudaError_t launch_partition(int elem_code, const PartitionLaunch& a, cudaStream_t s);
 
 }  // namespace bsg

@@ -635,3 +635,40 @@ def test_partitioned_full_32_bit_domain(bsg, cuda):
     assert np.array_equal(tail, O.shuffle_indices_range(m, 32, PHILOX, 24, m - 2048, m))
     del outs
     cuda.cuda.empty_cache()
+
+
+def test_partitioned_non_power_of_two(bsg, cuda):
+    """Non-power-of-two domains through the partitioned path (inputs routed by counter f^-1(j), windows compacted by
+    counter rank): equal to the oracle for both bijections, u64 and u32 payloads, ragged last tiles."""
+    for m, variant, dt in [((1 << 20) + 1, PHILOX, cuda.int64), ((1 << 20) + 1, LCG, cuda.int64),
+                           (3 * (1 << 18) + 17, PHILOX, cuda.int32), ((1 << 16) + 4097, PHILOX, cuda.int64),
+                           ((1 << 15) - 3, LCG, cuda.int32), ((1 << 21) - 1, PHILOX, cuda.int64)]:
+        vals = cuda.arange(m, dtype=dt, device="cuda")
+        old = bsg.set_path(2)
+        try:
+            out = bsg.shuffle_values(vals, cfg_of(bsg, seed=m, variant=variant))
+        finally:
+            bsg.set_path(old)
+        got = out.cpu().numpy().astype(np.int64).view(np.uint64) if dt == cuda.int32 else out.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, O.shuffle_indices(m, m, variant, 24)), (m, variant, dt)
+
+
+def test_partitioned_non_power_of_two_full_size(bsg, cuda):
+    """C3 itself (2^29+1 u64, 2^30 counters): the partitioned and single-pass paths agree bit for bit, for the
+    Feistel and the LCG; the head matches the oracle."""
+    m = (1 << 29) + 1
+    vals = cuda.arange(m, dtype=cuda.int64, device="cuda")
+    for variant in (PHILOX, LCG):
+        outs = []
+        for path in (2, 1):
+            old = bsg.set_path(path)
+            try:
+                outs.append(bsg.shuffle_values(vals, cfg_of(bsg, seed=0x5EED, variant=variant)))
+            finally:
+                bsg.set_path(old)
+        assert cuda.equal(outs[0], outs[1]), variant
+        exp = O.shuffle_indices_range(m, 0x5EED, variant, 24, 0, 8192)  # survivors of the first 8192 counters
+        assert np.array_equal(outs[0][:len(exp)].cpu().numpy().view(np.uint64), exp), variant
+        del outs
+    del vals
+    cuda.cuda.empty_cache()
