@@ -553,15 +553,14 @@ __global__ void __launch_bounds__(kP3Threads) k_place_compact(const T* __restric
   }
 }
 
-// Exclusive prefix of n u32 counts (one CTA; n <= 2^20 windows).
+// Window-count prefix, level 1: CTA k scans counts [1024k, 1024k + 1024) into pre[] (chunk-local exclusive
+// prefix) and writes the chunk total; level 2 (k_window_fix) adds the totals of the chunks before each one.
 __global__ void __launch_bounds__(1024) k_window_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pre,
-                                                     uint32_t n) {
+                                                     uint32_t* __restrict__ chunk_sum, uint32_t n) {
   __shared__ uint32_t wt[32];
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t per = (n + 1023) / 1024, b = tid * per;
-  uint32_t sum = 0;
-  for (uint32_t k = 0; k < per && b + k < n; ++k) sum += cnt[b + k];
-  uint32_t x = sum;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, i = blockIdx.x * 1024 + tid;
+  const uint32_t v = i < n ? cnt[i] : 0u;
+  uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
@@ -570,21 +569,33 @@ __global__ void __launch_bounds__(1024) k_window_scan(const uint32_t* __restrict
   if (lane == 31) wt[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t v = wt[lane];
-    uint32_t z = v;
+    const uint32_t t = wt[lane];
+    uint32_t z = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, o);
       if (lane >= static_cast<uint32_t>(o)) z += y;
     }
-    wt[lane] = z - v;
+    wt[lane] = z - t;
+    if (lane == 31) chunk_sum[blockIdx.x] = z;
   }
   __syncthreads();
-  uint32_t run = wt[warp] + x - sum;
-  for (uint32_t k = 0; k < per && b + k < n; ++k) {
-    pre[b + k] = run;
-    run += cnt[b + k];
+  if (i < n) pre[i] = wt[warp] + x - v;
+}
+
+__global__ void __launch_bounds__(1024) k_window_fix(uint32_t* __restrict__ pre,
+                                                    const uint32_t* __restrict__ chunk_sum, uint32_t n) {
+  __shared__ uint32_t off;
+  const uint32_t tid = threadIdx.x, i = blockIdx.x * 1024 + tid;
+  if (tid < 32) {
+    uint32_t acc = 0;
+    for (uint32_t j = tid; j < blockIdx.x; j += 32) acc += chunk_sum[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (tid == 0) off = acc;
   }
+  __syncthreads();
+  if (i < n) pre[i] += off;
 }
 
 template <typename T>
@@ -593,9 +604,12 @@ int window_log2() {
 }
 
 // Coarse/fine split of the bits above the window: (s1, s2) fan-outs.
+#ifndef BSG_PART_S1_BIAS
+#define BSG_PART_S1_BIAS 0
+#endif
 void part_split(int bits, int w2, int& s1, int& s2) {
   const int total = bits - w2;
-  s1 = (total + 1) / 2;
+  s1 = (total + 1) / 2 + BSG_PART_S1_BIAS;
   s2 = total - s1;
 }
 
@@ -666,12 +680,14 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
                                                                        pad ? cur1 : nullptr);
     if (pad) {
       const uint32_t nwin = static_cast<uint32_t>(n >> w2);
-      k_window_scan<<<1, 1024, 0, s>>>(cur2, a.win_prefix, nwin);
+      uint32_t* chunk_sum = a.win_prefix + (static_cast<size_t>(kMaxB1) * kMaxB2);
+      k_window_scan<<<(nwin + 1023) / 1024, 1024, 0, s>>>(cur2, a.win_prefix, chunk_sum, nwin);
+      if (nwin > 1024) k_window_fix<<<(nwin + 1023) / 1024, 1024, 0, s>>>(a.win_prefix, chunk_sum, nwin);
       const size_t smc = sm3 + (size_t{1} << w2);  // window + one flag byte per counter
       cudaFuncSetAttribute(k_place_compact<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smc));
       k_place_compact<T><<<nwin, kP3Threads, smc, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, w2,
                                                         static_cast<T*>(a.out));
-      note_launch(5);
+      note_launch(nwin > 1024 ? 6 : 5);
       return cudaGetLastError();
     }
   } else {
@@ -863,7 +879,7 @@ bool partition_eligible(int elem_code, int bits) {
     default: return false;
   }
   const int total = bits - w2;
-  const int s1 = (total + 1) / 2, s2 = total - s1;
+  const int s1 = (total + 1) / 2 + BSG_PART_S1_BIAS, s2 = total - s1;
   // fan-outs within the shared-memory histograms; tiles must not straddle buckets; 32-bit destinations
   return bits <= 32 && s1 >= 1 && s2 >= 1 && (1 << s1) <= kMaxB1 && (1 << s2) <= kMaxB2 &&
          (bits - s1) >= kP2TileLog && bits >= 14;
@@ -881,8 +897,8 @@ void partition_layout(int elem_code, int bits, bool pad, void* workspace, Partit
   P.cursors = reinterpret_cast<uint32_t*>(w);
   w += (kCursorWords * 4 + 255) / 256 * 256;
   if (pad) {
-    P.win_prefix = reinterpret_cast<uint32_t*>(w);
-    w += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 255) / 256 * 256;
+    P.win_prefix = reinterpret_cast<uint32_t*>(w);  // window prefix, then the scan's chunk totals
+    w += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 4096 + 255) / 256 * 256;
     P.tmp_values2 = w;
   }
 }
@@ -890,7 +906,7 @@ void partition_layout(int elem_code, int bits, bool pad, void* workspace, Partit
 size_t partition_workspace_bytes(int elem_code, int bits, bool pad) {
   const uint64_t n = 1ULL << bits;
   size_t b = n * static_cast<uint64_t>(elem_code) + n * 4 + n * 2 + (kCursorWords * 4 + 255) / 256 * 256;
-  if (pad) b += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 255) / 256 * 256 + n * static_cast<uint64_t>(elem_code);
+  if (pad) b += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 4096 + 255) / 256 * 256 + n * static_cast<uint64_t>(elem_code);
   return b;
 }
 
