@@ -283,12 +283,13 @@ def ours_arm(args, rank, world, local):
                                                       stream.cuda_stream), "shuffle_range")
                 dist.all_gather_into_tensor(counts, cnt_dev)  # the 8-byte count exchange (NCCL)
         pow2 = (m_total & (m_total - 1)) == 0
-        if not pow2:
+        partitioned = world == 1 and m_total * eb >= (256 << 20) and eb <= 8  # whole domain, >= 256 MiB
+        if partitioned:
+            dominant = "bsg::k_part1+k_part2t+k_place" if pow2 else "bsg::k_part1+k_part2t+k_place_compact"
+        elif not pow2:
             dominant = "bsg::k_compact_smem"
-        elif world == 1 and m_total * eb >= (256 << 20) and eb <= 8:
-            dominant = "bsg::k_part1+k_part2+k_place"  # partitioned path (whole domain, >= 256 MiB)
         else:
-            dominant = "bsg::k_pow2"  # counter-range shards take the single fused pass
+            dominant = "bsg::k_pow2"  # counter-range shards and 16-byte records take the single fused pass
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -462,7 +463,8 @@ def ours_arm(args, rank, world, local):
     alg_bytes = step_bytes_rank  # per launch on this rank (one kernel per step)
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
     prof = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
-    tkey = args.config + ("_single" if dominant == "bsg::k_pow2" and args.config == "c2" else "")
+    single = dominant in ("bsg::k_pow2", "bsg::k_compact_smem") and args.config in ("c2", "c3")
+    tkey = args.config + ("_single" if single else "")  # BSG_PATH=1 runs of the partitioned configurations
     traffic = prof.get(tkey, {}).get("dram_bytes_per_launch")
 
     line = {

@@ -11,7 +11,8 @@ for cfg in c2 c3 c4 c5; do
 done
 ncu --set full --clock-control none --import-source on -k regex:"k_part1|k_part2|k_place" -s 3 -c 3 -o $OUT/prof_c2 $B --config c2 > $OUT/prof_c2.log 2>&1
 BSG_PATH=1 ncu --set full --clock-control none --import-source on -k regex:k_pow2 -s 1 -c 1 -o $OUT/prof_c2single $B --config c2 > $OUT/prof_c2single.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_compact -s 1 -c 1 -o $OUT/prof_c3 $B --config c3 > $OUT/prof_c3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_part1|k_part2|k_window|k_place" -s 5 -c 5 -o $OUT/prof_c3 $B --config c3 > $OUT/prof_c3.log 2>&1
+BSG_PATH=1 ncu --set full --clock-control none --import-source on -k regex:k_compact -s 1 -c 1 -o $OUT/prof_c3single $B --config c3 > $OUT/prof_c3single.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_batched -s 1 -c 1 -o $OUT/prof_c4 $B --config c4 > $OUT/prof_c4.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pow2 -s 1 -c 1 -o $OUT/prof_c5 $B --config c5 > $OUT/prof_c5.log 2>&1
 ls -la $OUT
