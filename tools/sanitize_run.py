@@ -28,6 +28,10 @@ bsg.set_path(2)
 vals = torch.arange(1 << 16, dtype=torch.int64, device="cuda")
 check("partitioned", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=9)).cpu().numpy().view(np.uint64),
       O.shuffle_indices(1 << 16, 9))
+for m, v in (((1 << 16) + 5, 1), ((1 << 16) + 4099, 0), (1 << 16, 0)):  # padded / LCG (TMA-fed P1) partitions
+    vals = torch.arange(m, dtype=torch.int64, device="cuda")
+    check(f"partitioned {m} v{v}", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=7, variant=bsg.BijectionVariant(v))
+                                                      ).cpu().numpy().view(np.uint64), O.shuffle_indices(m, 7, v, 24))
 bsg.set_path(0)
 rows = torch.arange(1024, dtype=torch.int32, device="cuda").repeat(16, 1)
 out = bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=1000)).cpu().numpy()
