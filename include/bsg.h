@@ -190,10 +190,11 @@ uint64_t bsg_kernel_launches(void);
 /* Testing knob: 0 = automatic path choice, 1 = always use the compacting
  * (look-back) kernel even when every image survives. Returns the old value. */
 int32_t bsg_set_force_compact(int32_t on);
-/* Path selection for power-of-two shuffles: 0 = automatic (partitioned
- * three-pass kernel for payloads >= 256 MiB, single fused pass otherwise),
- * 1 = always the single fused pass, 2 = partitioned whenever eligible.
- * Outputs are identical; returns the old value. */
+/* Path selection for whole-domain shuffles: 0 = automatic (the partitioned
+ * kernels for payloads >= 256 MiB with elements of at most 8 bytes -- power of
+ * two or not -- and the single fused pass otherwise), 1 = always the single
+ * fused pass, 2 = partitioned whenever eligible (domains of 2^14..2^32
+ * counters).  Outputs are identical; returns the old value. */
 int32_t bsg_set_path(int32_t path);
 /* Release cached device/host workspaces of the current device. */
 bsg_status bsg_release_workspace(void);
