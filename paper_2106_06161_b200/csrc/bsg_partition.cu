@@ -656,16 +656,16 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
         static_cast<uint32_t>(full1));
     done1 = full1;
   }
-  if (done1 < tiles1) {
-    if (pad)
-      k_part1<KIND, D, T, true><<<static_cast<unsigned>(tiles1 - done1), kP1Threads, sm1, s>>>(
-          static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, m,
-          static_cast<uint32_t>(done1));
-    else
-      k_part1<KIND, D, T, false><<<static_cast<unsigned>(tiles1 - done1), kP1Threads, sm1, s>>>(
-          static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, m,
-          static_cast<uint32_t>(done1));
+  if (done1 < full1) {  // full tiles without the per-element bounds checks
+    k_part1<KIND, D, T, false><<<static_cast<unsigned>(full1 - done1), kP1Threads, sm1, s>>>(
+        static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, m,
+        static_cast<uint32_t>(done1));
+    done1 = full1;
   }
+  if (done1 < tiles1)  // the partial last tile of a non-power-of-two domain
+    k_part1<KIND, D, T, true><<<1, kP1Threads, sm1, s>>>(static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p,
+                                                         b - s1, nb1, w1, a.dest_in, m,
+                                                         static_cast<uint32_t>(done1));
   // P2 writes the fine windows into `out` itself (power of two: exact sizes) or into a counter-sized buffer.
   T* p2out = pad ? static_cast<T*>(a.tmp_values2) : static_cast<T*>(a.out);
   if constexpr (sizeof(T) <= 8) {  // TMA-fed persistent P2 (2.65 -> 2.45 ms for C2); 16-byte records keep k_part2
