@@ -643,9 +643,10 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   // Cheap destinations (LCG, a given permutation) leave P1 bound by its loads: the TMA-fed persistent P1 (2 CTAs
   // per SM) hides them (C2 LCG 7.69 -> 7.07 ms).  The 24-round Philox needs the third CTA per SM of k_part1 to
   // keep the integer pipes busy (k_part1t: 5.16 vs 3.97 ms).
+  // With 512 coarse buckets (domains of 2^30+) the 2-CTA TMA-fed form loses (C3-LCG P1 4.72 vs 4.05 ms).
   constexpr bool kTmaP1 = (KIND == kKindLcg || KIND == kKindDestArray) && sizeof(T) <= 8;
   uint64_t done1 = 0;
-  if (kTmaP1 && full1 > 0) {
+  if (kTmaP1 && full1 > 0 && nb1 <= 256) {
     const size_t smt = kP1Tile * (2 * sizeof(T) + 4);
     cudaFuncSetAttribute(k_part1t<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
     int per = 1;
