@@ -576,7 +576,8 @@ def test_cuda_graph_capture_and_replay(bsg, cuda):
     every replay recomputes the shuffle of the input's current contents -- including the look-back path,
     whose status words a replay cannot re-epoch, and generic round counts, whose keys a replay re-uploads."""
     cases = [((1 << 20), 24, cuda.int64, "pow2"), ((1 << 20) + 7, 24, cuda.int64, "lookback"),
-             ((1 << 16) + 1, 9, cuda.int32, "generic rounds"), ((1 << 25), 24, cuda.int64, "partitioned")]
+             ((1 << 16) + 1, 9, cuda.int32, "generic rounds"), ((1 << 25), 24, cuda.int64, "partitioned"),
+             ((1 << 25) + 3, 24, cuda.int64, "partitioned")]  # padded: window scan + compaction in the graph
     for m, rounds, dt, what in cases:
         cfg = cfg_of(bsg, seed=77, rounds=rounds)
         vals = cuda.arange(m, dtype=dt, device="cuda")
