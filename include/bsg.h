@@ -196,7 +196,10 @@ int32_t bsg_set_force_compact(int32_t on);
  * fused pass, 2 = partitioned whenever eligible (domains of 2^14..2^32
  * counters).  Outputs are identical; returns the old value. */
 int32_t bsg_set_path(int32_t path);
-/* Release cached device/host workspaces of the current device. */
+/* Release cached device/host workspaces of the current device.  CUDA graphs
+ * captured from libbsg calls reference these workspaces and must not be
+ * replayed afterwards (growing a workspace, by contrast, keeps the old one
+ * alive for such graphs). */
 bsg_status bsg_release_workspace(void);
 
 #if defined(__GNUC__)

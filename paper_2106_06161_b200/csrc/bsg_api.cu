@@ -49,8 +49,18 @@ bsg_status fail(bsg_status s, const std::string& msg) {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  // Set when a captured CUDA graph references the buffer: growing it then retires the old allocation instead of
+  // freeing it, so the graph stays valid (retired buffers are freed with the buffer's owner).
+  bool captured = false;
+  std::vector<void*> retired;
   cudaError_t ensure(size_t n, bool zero = false) {
     if (bytes >= n && p) return cudaSuccess;
+    if (captured && p) {
+      retired.push_back(p);
+      p = nullptr;
+      bytes = 0;
+      captured = false;
+    }
     release();
     size_t want = std::max<size_t>(n, 256);
     cudaError_t e = cudaMalloc(&p, want);
@@ -66,6 +76,12 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
+  }
+  void release_all() {  // also the retired allocations (bsg_release_workspace: no graph may replay afterwards)
+    release();
+    for (void* q : retired) cudaFree(q);
+    retired.clear();
+    captured = false;
   }
 };
 
@@ -189,6 +205,7 @@ bsg_status upload_keys(DeviceCtx* c, BijParams& p, uint64_t seed, cudaStream_t s
   if (capturing(s)) {
     // the graph's copy node reads this host array at every replay: keep it for the context's lifetime
     if (c->keys.bytes < k.size() * 4) return fail(BSG_EINVAL, "graph capture: run this call once uncaptured first");
+    c->keys.captured = true;
     c->captured_keys.push_back(std::move(k));
     const std::vector<uint32_t>& kk = c->captured_keys.back();
     BSG_CUDA(cudaMemcpyAsync(c->keys.p, kk.data(), kk.size() * 4, cudaMemcpyHostToDevice, s));
@@ -210,6 +227,7 @@ bsg_status lookback_prepare(DeviceCtx* c, uint64_t tiles, cudaStream_t s, bsg::L
     // A replayed graph cannot advance the epoch: it clears its status words and uses epoch 1, which
     // uncaptured launches never use.
     if (c->status.bytes < need) return fail(BSG_EINVAL, "graph capture: run this call once uncaptured first");
+    c->status.captured = true;
     BSG_CUDA(cudaMemsetAsync(c->status.p, 0, need, s));
     lb.epoch = 1;
     return BSG_OK;
@@ -251,8 +269,12 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
       (pow2 || elem_code <= 8) && bsg::partition_eligible(elem_code, bits) &&
       auto_partition(m, static_cast<uint64_t>(elem_code))) {
     const size_t need = bsg::partition_workspace_bytes(elem_code, bits, !pow2);
-    cudaError_t ae = c->part.ensure(need);
+    // while capturing, never allocate (it would invalidate the capture): use the workspace only if it is sized
+    const bool cap = capturing(s);
+    const cudaError_t ae = cap ? (c->part.p && c->part.bytes >= need ? cudaSuccess : cudaErrorNotReady)
+                               : c->part.ensure(need);
     if (ae == cudaSuccess) {
+      if (cap) c->part.captured = true;
       bsg::PartitionLaunch P;
       bsg::partition_layout(elem_code, bits, !pow2, c->part.p, P);
       P.in = src.base;
@@ -736,7 +758,8 @@ bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uin
     const bool pow2 = (1ULL << bits) == n;
     if (pow2 && g_path != 1 && bsg::partition_eligible(code, bits) &&
         (g_path == 2 || n * static_cast<uint64_t>(elem_bytes) >= g_partition_min_bytes) &&
-        c->part.ensure(bsg::partition_workspace_bytes(code, bits)) == cudaSuccess) {
+        (capturing(s) ? (c->part.p && c->part.bytes >= bsg::partition_workspace_bytes(code, bits))
+                      : c->part.ensure(bsg::partition_workspace_bytes(code, bits)) == cudaSuccess)) {
       bsg::PartitionLaunch P;
       bsg::partition_layout(code, bits, false, c->part.p, P);
       P.in = values;
@@ -925,13 +948,13 @@ int32_t bsg_set_force_compact(int32_t on) {
 bsg_status bsg_release_workspace(void) {
   return with_ctx([&](DeviceCtx* c) -> bsg_status {
     BSG_CUDA(cudaDeviceSynchronize());
-    c->status.release();
-    c->keys.release();
-    c->st_in.release();
-    c->st_out.release();
-    c->st_idx.release();
-    c->st_tmp.release();
-    c->part.release();
+    c->status.release_all();  // graphs captured earlier must not be replayed after this
+    c->keys.release_all();
+    c->st_in.release_all();
+    c->st_out.release_all();
+    c->st_idx.release_all();
+    c->st_tmp.release_all();
+    c->part.release_all();
     c->epoch = 0;
     return BSG_OK;
   });

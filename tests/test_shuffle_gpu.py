@@ -673,3 +673,30 @@ def test_partitioned_non_power_of_two_full_size(bsg, cuda):
         del outs
     del vals
     cuda.cuda.empty_cache()
+
+
+def test_cuda_graph_survives_workspace_growth(bsg, cuda):
+    """A graph captured with the partition workspace sized for 2^22 stays valid after an uncaptured 2^24 call
+    grows the workspace (the captured allocation is retired, not freed)."""
+    m = (1 << 22) + 1
+    cfg = cfg_of(bsg, seed=3)
+    vals = cuda.arange(m, dtype=cuda.int64, device="cuda")
+    out = cuda.empty_like(vals)
+    old = bsg.set_path(2)
+    try:
+        bsg.shuffle_values_into(vals, cfg, out)
+        g = cuda.cuda.CUDAGraph()
+        s = cuda.cuda.Stream()
+        with cuda.cuda.stream(s):
+            cuda.cuda.synchronize()
+            with cuda.cuda.graph(g, stream=s):
+                bsg.shuffle_values_into(vals, cfg, out)
+        big = cuda.arange((1 << 24) + 1, dtype=cuda.int64, device="cuda")
+        bsg.shuffle_values(big, cfg)  # grows the cached workspace
+        del big
+        out.zero_()
+        g.replay()
+        cuda.cuda.synchronize()
+        assert cuda.equal(out, bsg.shuffle_values(vals, cfg))
+    finally:
+        bsg.set_path(old)
