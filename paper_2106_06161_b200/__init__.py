@@ -374,7 +374,8 @@ def kernel_launches() -> int:
 
 
 def set_path(path: int) -> int:
-    """0 = automatic, 1 = single fused pass only, 2 = partitioned three-pass whenever eligible (pow2)."""
+    """0 = automatic, 1 = single fused pass only, 2 = partitioned passes whenever eligible (whole domains of
+    2^14..2^32 counters; non-power-of-two domains for elements of at most 8 bytes).  Outputs are identical."""
     return int(lib.bsg_set_path(int(path)))
 
 
