@@ -493,6 +493,20 @@ def ours_arm(args, rank, world, local):
         # how close the kernels run to their own physical DRAM traffic at the measured peak
         line["roofline"]["traffic_floor_ms"] = round(traffic / (peak * 1e9) * 1e3, 4)
         line["roofline"]["frac_of_traffic_floor"] = round(traffic / (peak * 1e9) * 1e3 / kernel_ms, 4)
+    if dominant.startswith("bsg::k_part1") and variant == 1:
+        # Composite floor of the partitioned path: P1 cannot beat the 24-round inverse
+        # cipher on the FMA-heavy pipe (IMAD + IMAD.HI + IMAD = 8 issue cycles per round per warp, measured in
+        # tools/microbench/mb8.cu) nor its own traffic; P2 and P3 cannot beat their traffic at the HBM peak.
+        sms, hz = 148, (clk.summary().get("sm_mhz") or 1965) * 1e6
+        cipher_ms = m_total * 24 * 8 / 32 / (sms * 4 * hz) * 1e3
+        p1_bytes, p23_bytes = m_total * (eb + eb + 4), m_total * ((eb + 4) + (eb + 2) + (eb + 2) + eb)
+        p1_ms = max(cipher_ms, p1_bytes / (peak * 1e9) * 1e3)
+        comp = p1_ms + p23_bytes / (peak * 1e9) * 1e3
+        line["roofline"]["composite_floor"] = {
+            "cipher_ms": round(cipher_ms, 3), "p1_traffic_ms": round(p1_bytes / (peak * 1e9) * 1e3, 3),
+            "p2_p3_traffic_ms": round(p23_bytes / (peak * 1e9) * 1e3, 3), "floor_ms": round(comp, 3),
+            "frac": round(comp / kernel_ms, 4),
+            "what": "max(P1 inverse-cipher issue floor, P1 traffic) + P2/P3 traffic at the HBM peak"}
     if not args.no_comparators and world == 1 and not batch:
         line["comparators"] = comparators(bsg, torch, dev, vals, out, m_total, eb, cfg, stream)
         gb = line["comparators"].get("gather_bound", {}).get("value")
