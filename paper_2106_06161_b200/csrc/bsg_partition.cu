@@ -1,28 +1,31 @@
-// bsg_partition.cu -- partitioned (three-pass) shuffle for large power-of-two
-// domains, the B200 answer to the DRAM random-access wall.
+// bsg_partition.cu -- partitioned (three-pass) shuffle for large domains, the
+// B200 answer to the DRAM random-access wall.
 //
 // Why: a single-pass shuffle of a 4 GiB array issues one random read per
 // element; on B200 those saturate at ~47 G reads/s (DRAM row activations,
 // independent of element size -- profiles/r01_microbench.md), i.e. 11.4 ms for
-// 2^29 elements although 8.6 GB of payload would stream in 1.4 ms.  When
-// m == 2^bits every counter survives and out[f^-1(j)] = in[j], so the
-// permutation can be applied by streaming the INPUT in order and routing each
-// element by its destination f^-1(j) (philox_invert, bijection.hpp:117-143):
-//   P1  read in[] sequentially, inverse cipher -> dest, counting-sort each
-//       4096-element tile in shared memory into 2^s1 coarse destination
-//       buckets, append the runs to the buckets (value + u32 dest);
+// 2^29 elements although 8.6 GB of payload would stream in 1.4 ms.  Every
+// input j < m has exactly one counter c = f^-1(j) (philox_invert,
+// bijection.hpp:117-143) and lands at the rank of c among the survivors; when
+// m == 2^bits that rank is c itself.  So the permutation is applied by
+// streaming the INPUT in order and routing each element by c:
+//   P1  read in[] sequentially, inverse cipher -> c, counting-sort each
+//       4096-element tile in shared memory into 2^s1 coarse counter buckets,
+//       append the runs to the buckets (value + u32 c);
 //   P2  per coarse bucket, the same split into 2^s2 fine windows of W2
-//       elements (value + u16 dest-in-window), written into `out` itself;
-//   P3  per fine window (64 KiB), scatter into shared memory at dest and
-//       write the window back coalesced (in place: each CTA reads its whole
-//       range before writing).
+//       counters (value + u16 offset in the window), written into `out`
+//       itself (power of two) or into a counter-sized buffer (padded domain);
+//   P3  per fine window (64 KiB), scatter into shared memory by offset and
+//       write the window back coalesced: in place (power of two), or compacted
+//       in counter order at the window's prefix of survivor counts (padded,
+//       k_place_compact after the two-level k_window_scan/fix).
 // Every DRAM access is a coalesced run; traffic is ~60 B/element instead of
 // one random 64-B access per 8-B element.  P2 (and P1 for cheap bijections)
-// run persistent with TMA bulk copies of the next tile in flight.  P1 for the
-// 24-round Philox is bound by the integer pipes (the cipher).  Exact sizes (pow2: each bucket
-// receives exactly its window) make the layout static; atomic cursors only
-// order elements inside a bucket, which the final exact placement makes
-// irrelevant -- the output is bit-identical to the single-pass kernel.
+// run persistent with TMA bulk copies of the next tile in flight; P1 for the
+// 24-round Philox is bound by the integer pipes (the cipher).  Bucket and
+// window capacities are counter ranges, so the layout is static; atomic
+// cursors only order elements inside a bucket, which the final placement by
+// counter makes irrelevant -- the output is bit-identical to the single pass.
 #include <cuda_runtime.h>
 
 #include <algorithm>
