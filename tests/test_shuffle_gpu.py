@@ -700,3 +700,25 @@ def test_cuda_graph_survives_workspace_growth(bsg, cuda):
         assert cuda.equal(out, bsg.shuffle_values(vals, cfg))
     finally:
         bsg.set_path(old)
+
+
+def test_partitioned_random_shapes(bsg, cuda):
+    """Randomised parity of the forced partitioned path (power of two or not, both bijections, u32/u64, generic
+    round counts) against the oracle."""
+    rng = np.random.default_rng(2106)
+    old = bsg.set_path(2)
+    try:
+        for _ in range(24):
+            m = int(rng.integers(1 << 14, 1 << 21))
+            if rng.random() < 0.25:
+                m = 1 << int(m.bit_length() - 1)
+            variant = int(rng.integers(0, 2))
+            rounds = int(rng.choice([24, 24, 7, 30]))
+            seed = int(rng.integers(0, 2**63))
+            dt = cuda.int64 if rng.random() < 0.5 else cuda.int32
+            vals = cuda.arange(m, dtype=dt, device="cuda")
+            out = bsg.shuffle_values(vals, cfg_of(bsg, seed=seed, variant=variant, rounds=rounds))
+            got = out.cpu().numpy().astype(np.int64).view(np.uint64)
+            assert np.array_equal(got, O.shuffle_indices(m, seed, variant, rounds)), (m, seed, variant, rounds, dt)
+    finally:
+        bsg.set_path(old)
