@@ -2,7 +2,7 @@
  * bsg.h -- C ABI of the B200-native bijective shuffle (libbsg.so).
  *
  * Drop-in boundary for the CPU path of the reference library `bijshuf`
- * (proj/include/bijshuf/*.hpp).  The reference has no FFI of its own: its
+ * (proj/include/bijshuf/ headers).  The reference has no FFI of its own: its
  * surface is header-only C++ templates.  Each entry point below replaces the
  * reference function cited beside it, with plain pointers and sizes, no C++
  * or torch types, and status codes instead of exceptions.  The C++ shim

@@ -28,6 +28,11 @@
 #else
 #define BSG_HD inline
 #endif
+#ifdef __CUDA_ARCH__
+#define BSG_UNROLL _Pragma("unroll")
+#else
+#define BSG_UNROLL
+#endif
 
 namespace bsg {
 
@@ -143,7 +148,7 @@ BSG_HD uint64_t philox_fwd(uint64_t x, const BijParams& p) {
   uint32_t s0 = static_cast<uint32_t>(x >> p.R);
   uint32_t s1 = static_cast<uint32_t>(x) & p.RM;
   if constexpr (NR > 0) {
-#pragma unroll
+    BSG_UNROLL
     for (int i = 0; i < NR; ++i) philox_round<D>(s0, s1, p.keys[i], p.L, p.LM, p.RM);
   } else {
 #ifdef __CUDA_ARCH__
@@ -224,7 +229,7 @@ template <int D, int NR>
 BSG_HD uint32_t philox_fwd32(uint32_t x, const BijParams& p) {
   uint32_t s0 = x >> p.R;
   uint32_t s1 = x & p.RM;
-#pragma unroll
+  BSG_UNROLL
   for (int i = 0; i < NR; ++i) philox_round<D>(s0, s1, p.keys[i], p.L, p.LM, p.RM);
   return (s0 << p.R) | (s1 & p.RM);
 }
