@@ -18,6 +18,7 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <variant>
 #include <vector>
 
 namespace bijshuf {
@@ -62,17 +63,48 @@ inline bsg_config to_c(const ShuffleConfig& c) {
 }  // namespace detail
 
 // ------------------------------------------------------------- splitmix.hpp
-inline std::uint64_t mix64(std::uint64_t z) { return bsg_mix64(z); }
+// mix64 stays constexpr (the reference's is): it is the same three-line
+// finalizer libbsg evaluates (bsg_mix64), checked equal in tests/cpp.
+constexpr std::uint64_t mix64(std::uint64_t z) noexcept {  // splitmix.hpp:11-15
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
 inline constexpr std::uint64_t kSplitMixGamma = 0x9E3779B97F4A7C15ULL;
-inline std::vector<std::uint32_t> derive_round_keys(std::uint64_t seed, int num_rounds) {
+inline std::vector<std::uint32_t> derive_round_keys(std::uint64_t seed, int num_rounds) {  // splitmix.hpp:22-31
   if (num_rounds < 1) throw std::invalid_argument("num_rounds must be >= 1");
   std::vector<std::uint32_t> k(static_cast<std::size_t>(num_rounds));
   detail::throw_on(bsg_derive_round_keys(seed, num_rounds, k.data()), "derive_round_keys");
   return k;
 }
 
+// splitmix.hpp:35-63: value k of stream s is mix64(s + k * gamma).
+class SplitMix64 {
+ public:
+  using result_type = std::uint64_t;
+  explicit constexpr SplitMix64(std::uint64_t seed) noexcept : state_(seed) {}
+  constexpr std::uint64_t operator()() noexcept {
+    state_ += kSplitMixGamma;
+    return mix64(state_);
+  }
+  static constexpr std::uint64_t min() noexcept { return 0; }
+  static constexpr std::uint64_t max() noexcept { return ~0ULL; }
+  // Unbiased draw from [0, bound) by rejection of the uneven tail; bound >= 1.
+  std::uint64_t below(std::uint64_t bound) {
+    if (bound == 0) throw std::invalid_argument("bound must be >= 1");
+    const std::uint64_t limit = ~0ULL - (~0ULL % bound);
+    for (;;) {
+      const std::uint64_t v = (*this)();
+      if (v < limit) return v % bound;
+    }
+  }
+
+ private:
+  std::uint64_t state_;
+};
+
 // ------------------------------------------------------------ bijection.hpp
-struct LcgParams {
+struct LcgParams {  // bijection.hpp:14-22
   int modulus_bits = 0;
   std::uint64_t a = 1;
   std::uint64_t c = 0;
@@ -81,20 +113,20 @@ struct LcgParams {
   }
 };
 
-inline LcgParams make_lcg(int modulus_bits, std::uint64_t seed) {
+inline LcgParams make_lcg(int modulus_bits, std::uint64_t seed) {  // bijection.hpp:25-34
   LcgParams p;
   p.modulus_bits = modulus_bits;
   detail::throw_on(bsg_make_lcg(modulus_bits, seed, &p.a, &p.c), "make_lcg");
   return p;
 }
 
-inline std::uint64_t lcg_apply(const LcgParams& p, std::uint64_t x) {
+inline std::uint64_t lcg_apply(const LcgParams& p, std::uint64_t x) {  // bijection.hpp:36-40
   std::uint64_t y = 0;
   detail::throw_on(bsg_lcg_apply(p.modulus_bits, p.a, p.c, x, &y), "lcg_apply");
   return y;
 }
 
-struct VariablePhiloxParams {
+struct VariablePhiloxParams {  // bijection.hpp:45-53
   int total_bits = 0;
   int left_side_bits = 0;
   int right_side_bits = 0;
@@ -102,10 +134,24 @@ struct VariablePhiloxParams {
   std::uint64_t left_side_mask = 0;
   std::uint64_t right_side_mask = 0;
   std::vector<std::uint32_t> round_keys;
-  std::uint64_t seed = 0;  // keys are derived from it (derive_round_keys)
 };
 
-inline VariablePhiloxParams make_philox(int total_bits, std::uint64_t seed, int num_rounds = 24) {
+namespace detail {
+inline bsg_philox_params to_c(const VariablePhiloxParams& p) {
+  bsg_philox_params c;
+  c.total_bits = p.total_bits;
+  c.left_side_bits = p.left_side_bits;
+  c.right_side_bits = p.right_side_bits;
+  c.num_rounds = p.num_rounds;
+  c.left_side_mask = p.left_side_mask;
+  c.right_side_mask = p.right_side_mask;
+  c.round_keys = p.round_keys.data();
+  c.num_keys = p.round_keys.size();
+  return c;
+}
+}  // namespace detail
+
+inline VariablePhiloxParams make_philox(int total_bits, std::uint64_t seed, int num_rounds = 24) {  // :73-88
   if (total_bits < 2 || total_bits > 63) throw std::invalid_argument("total_bits must be in [2, 63]");
   if (num_rounds < 3) throw std::invalid_argument("num_rounds must be >= 3");
   VariablePhiloxParams p;
@@ -116,20 +162,36 @@ inline VariablePhiloxParams make_philox(int total_bits, std::uint64_t seed, int 
   p.left_side_mask = (1ULL << p.left_side_bits) - 1;
   p.right_side_mask = (1ULL << p.right_side_bits) - 1;
   p.round_keys = derive_round_keys(seed, num_rounds);
-  p.seed = seed;
   return p;
 }
 
-inline std::uint64_t philox_apply(const VariablePhiloxParams& p, std::uint64_t x) {
+// Both directions honour every field of p (round_keys, num_rounds including 0, the side widths and masks).
+inline std::uint64_t philox_apply(const VariablePhiloxParams& p, std::uint64_t x) {  // bijection.hpp:94-111
+  const bsg_philox_params c = detail::to_c(p);
   std::uint64_t y = 0;
-  detail::throw_on(bsg_philox_apply(p.total_bits, p.seed, p.num_rounds, x, &y), "philox_apply");
+  detail::throw_on(bsg_philox_apply_params(&c, x, &y), "philox_apply");
   return y;
 }
 
-inline std::uint64_t philox_invert(const VariablePhiloxParams& p, std::uint64_t y) {
+inline std::uint64_t philox_invert(const VariablePhiloxParams& p, std::uint64_t y) {  // bijection.hpp:117-143
+  const bsg_philox_params c = detail::to_c(p);
   std::uint64_t x = 0;
-  detail::throw_on(bsg_philox_invert(p.total_bits, p.seed, p.num_rounds, y, &x), "philox_invert");
+  detail::throw_on(bsg_philox_invert_params(&c, y, &x), "philox_invert");
   return x;
+}
+
+// bijection.hpp:146-169: tagged choice between the two families.
+struct BijectionSpec {
+  std::variant<LcgParams, VariablePhiloxParams> variant;
+  int domain_bits = 0;
+};
+
+inline BijectionSpec make_bijection(const LcgParams& p) { return BijectionSpec{p, p.modulus_bits}; }
+inline BijectionSpec make_bijection(const VariablePhiloxParams& p) { return BijectionSpec{p, p.total_bits}; }
+
+inline std::uint64_t bijection_apply(const BijectionSpec& spec, std::uint64_t x) {
+  if (const LcgParams* l = std::get_if<LcgParams>(&spec.variant)) return lcg_apply(*l, x);
+  return philox_apply(std::get<VariablePhiloxParams>(spec.variant), x);
 }
 
 // -------------------------------------------------------------- shuffle.hpp

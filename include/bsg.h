@@ -72,6 +72,26 @@ bsg_status bsg_lcg_apply(int32_t bits, uint64_t a, uint64_t c, uint64_t x, uint6
 /* make_philox + philox_apply / philox_invert, bijection.hpp:73-143 (host scalar) */
 bsg_status bsg_philox_apply(int32_t bits, uint64_t seed, int32_t rounds, uint64_t x, uint64_t* y);
 bsg_status bsg_philox_invert(int32_t bits, uint64_t seed, int32_t rounds, uint64_t y, uint64_t* x);
+/* VariablePhiloxParams (bijection.hpp:45-53) exactly as the caller holds
+ * them -- from make_philox or assembled field by field (the reference's
+ * ZeroRoundsIsIdentity tests set num_rounds = 0 by hand).  The two calls below
+ * evaluate philox_apply / philox_invert (bijection.hpp:94-143) from these
+ * fields alone: caller-edited round_keys and round counts are honoured.
+ * ERANGE for an input outside [0, 2^total_bits) (total_bits < 64); EINVAL
+ * for fields the reference's arithmetic is undefined on (side widths outside
+ * [0, 63], right_side_bits < left_side_bits, fewer keys than rounds). */
+typedef struct {
+  int32_t total_bits;
+  int32_t left_side_bits;
+  int32_t right_side_bits;
+  int32_t num_rounds;
+  uint64_t left_side_mask;
+  uint64_t right_side_mask;
+  const uint32_t* round_keys; /* num_keys entries; may be NULL when num_rounds <= 0 */
+  uint64_t num_keys;
+} bsg_philox_params;
+bsg_status bsg_philox_apply_params(const bsg_philox_params* p, uint64_t x, uint64_t* y);
+bsg_status bsg_philox_invert_params(const bsg_philox_params* p, uint64_t y, uint64_t* x);
 /* Batched evaluation on the GPU: y[i] = f(x[i]) (inverse != 0: f^-1).
  * x == NULL evaluates the counters start .. start+n-1.  ERANGE if an input
  * lies outside the domain (checked on the host for host inputs only). */
@@ -154,8 +174,13 @@ bsg_status bsg_route_by_dest(const void* in, uint64_t n_local, uint64_t global_o
 bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uint64_t n, void* out,
                                    uint32_t elem_bytes, void* stream);
 
-/* CUDA IPC helpers for sharded inputs across processes (one process per GPU). */
-#define BSG_IPC_HANDLE_BYTES 64
+/* CUDA IPC helpers for sharded inputs across processes (one process per GPU).
+ * The exported handle carries the CUDA IPC handle of the allocation that
+ * contains dev_ptr plus dev_ptr's offset inside it (pointers from a caching
+ * allocator such as PyTorch's usually sit inside a larger segment), so
+ * bsg_ipc_open returns the peer's address of dev_ptr itself.  bsg_ipc_close
+ * takes that returned pointer. */
+#define BSG_IPC_HANDLE_BYTES 80
 bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_HANDLE_BYTES]);
 bsg_status bsg_ipc_open(const unsigned char handle[BSG_IPC_HANDLE_BYTES], void** dev_ptr_out);
 bsg_status bsg_ipc_close(void* dev_ptr);
@@ -196,6 +221,11 @@ int32_t bsg_set_force_compact(int32_t on);
  * fused pass, 2 = partitioned whenever eligible (domains of 2^14..2^32
  * counters).  Outputs are identical; returns the old value. */
 int32_t bsg_set_path(int32_t path);
+/* Bytes of device memory the library currently holds as cached workspaces on
+ * the current device (the partitioned path keeps ~14 B per counter for power-of-two
+ * domains and ~22 B per counter for padded ones between calls: 7.5 GB after a
+ * 2^29-element u64 shuffle).  bsg_release_workspace() returns them. */
+bsg_status bsg_workspace_bytes(uint64_t* bytes);
 /* Release cached device/host workspaces of the current device.  CUDA graphs
  * captured from libbsg calls reference these workspaces and must not be
  * replayed afterwards (growing a workspace, by contrast, keeps the old one

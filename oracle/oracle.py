@@ -89,6 +89,7 @@ def _load_ref():
         "ref_time_shuffle_u64_calls": (c_int, [c_uint64, c_uint64, c_int, c_int, c_int, c_int, c_void_p,
                                                POINTER(c_uint64)]),
         "ref_time_shuffle_pairs_calls": (c_int, [c_uint64, c_uint64, c_int, c_int, c_int, c_int, c_void_p]),
+        "ref_time_batched_u32_calls": (c_int, [c_uint64, c_uint64, c_uint64, c_int, c_int, c_int, c_int, c_void_p]),
     }
     for k, (r, a) in sig.items():
         f = getattr(lib, k)

@@ -208,4 +208,30 @@ int ref_time_shuffle_pairs_calls(uint64_t m, uint64_t seed, int variant, int rou
   });
 }
 
+// C4 payload: `batch` independent shuffles of iota(m) u32 rows keyed seed + b -- the
+// BijectiveShuffleSampler convention (stats.hpp:314-324) with the values moved by
+// shuffle_values_into (shuffle.hpp:308-315).  The reference runs one shuffle per
+// call (m = 1024 is one 65536-counter chunk, so one worker); the rows are spread
+// over `threads` host threads (0 = hardware_concurrency).  Each call of the batch
+// is timed individually into per_call_s[0..calls).
+int ref_time_batched_u32_calls(uint64_t batch, uint64_t m, uint64_t seed, int variant, int rounds, int threads,
+                               int calls, double* per_call_s) {
+  return guarded([&] {
+    const int T = threads > 0 ? threads : resolve_workers(0);
+    std::vector<std::vector<uint32_t>> in(batch, std::vector<uint32_t>(m)), out(batch, std::vector<uint32_t>(m));
+    for (auto& r : in) std::iota(r.begin(), r.end(), uint32_t{0});
+    for (int t = 0; t < calls; ++t) {
+      const double t0 = now_s();
+      std::vector<std::thread> pool;
+      for (int w = 0; w < T; ++w)
+        pool.emplace_back([&, w] {
+          for (uint64_t b = w; b < batch; b += static_cast<uint64_t>(T))
+            shuffle_values_into(in[b], make_cfg(seed + b, variant, rounds, 1), out[b]);
+        });
+      for (auto& th : pool) th.join();
+      per_call_s[t] = now_s() - t0;
+    }
+  });
+}
+
 }  // extern "C"

@@ -42,6 +42,7 @@ __all__ = [
     "shuffle_values", "shuffle_values_into", "shuffle_values_batched", "gather", "gather_into",
     "compact_permutation", "mix64", "derive_round_keys", "LcgParams", "make_lcg", "lcg_apply",
     "VariablePhiloxParams", "make_philox", "philox_apply", "philox_invert", "bijection_apply", "sort_shuffle_u64",
+    "SplitMix64", "BijectionSpec", "make_bijection", "workspace_bytes", "release_workspace",
     "kernel_launches", "Pipeline", "BsgError", "CudaError", "InvalidArgument", "OutOfRange", "Permutation",
 ]
 
@@ -165,15 +166,22 @@ def lcg_apply(p: LcgParams, x: int) -> int:  # bijection.hpp:36-40
 
 
 @dataclass
-class VariablePhiloxParams:  # bijection.hpp:45-53 (keys derived from `seed`)
-    total_bits: int
-    left_side_bits: int
-    right_side_bits: int
-    num_rounds: int
-    left_side_mask: int
-    right_side_mask: int
+class VariablePhiloxParams:  # bijection.hpp:45-53
+    total_bits: int = 0
+    left_side_bits: int = 0
+    right_side_bits: int = 0
+    num_rounds: int = 0
+    left_side_mask: int = 0
+    right_side_mask: int = 0
     round_keys: List[int] = field(default_factory=list)
-    seed: int = 0
+
+    def _c(self):
+        keys = (ctypes.c_uint32 * max(1, len(self.round_keys)))(*[k & 0xFFFFFFFF for k in self.round_keys])
+        p = _lib.bsg_philox_params(self.total_bits, self.left_side_bits, self.right_side_bits, self.num_rounds,
+                                   self.left_side_mask & 0xFFFFFFFFFFFFFFFF, self.right_side_mask & 0xFFFFFFFFFFFFFFFF,
+                                   ctypes.cast(keys, ctypes.POINTER(ctypes.c_uint32)), len(self.round_keys))
+        p._keep = keys
+        return p
 
 
 def make_philox(total_bits: int, seed: int, num_rounds: int = 24) -> VariablePhiloxParams:  # bijection.hpp:73-88
@@ -184,28 +192,86 @@ def make_philox(total_bits: int, seed: int, num_rounds: int = 24) -> VariablePhi
     L = total_bits // 2
     R = total_bits - L
     return VariablePhiloxParams(total_bits, L, R, num_rounds, (1 << L) - 1, (1 << R) - 1,
-                                derive_round_keys(seed, num_rounds), seed & 0xFFFFFFFFFFFFFFFF)
+                                derive_round_keys(seed, num_rounds))
 
 
-def philox_apply(p: VariablePhiloxParams, x: int) -> int:  # bijection.hpp:94-111
-    if x < 0 or (x >> p.total_bits) != 0:
+def philox_apply(p: VariablePhiloxParams, x: int) -> int:  # bijection.hpp:94-111 (honours every field of p)
+    if x < 0 or (p.total_bits < 64 and (x >> p.total_bits) != 0):
         raise OutOfRange("philox_apply: x outside [0, 2^total_bits)")
     y = ctypes.c_uint64()
-    check(lib.bsg_philox_apply(p.total_bits, p.seed, p.num_rounds, x, ctypes.byref(y)), "philox_apply")
+    check(lib.bsg_philox_apply_params(ctypes.byref(p._c()), x, ctypes.byref(y)), "philox_apply")
     return y.value
 
 
-def philox_invert(p: VariablePhiloxParams, y: int) -> int:  # bijection.hpp:117-143
-    if y < 0 or (y >> p.total_bits) != 0:
+def philox_invert(p: VariablePhiloxParams, y: int) -> int:  # bijection.hpp:117-143 (honours every field of p)
+    if y < 0 or (p.total_bits < 64 and (y >> p.total_bits) != 0):
         raise OutOfRange("philox_invert: y outside [0, 2^total_bits)")
     x = ctypes.c_uint64()
-    check(lib.bsg_philox_invert(p.total_bits, p.seed, p.num_rounds, y, ctypes.byref(x)), "philox_invert")
+    check(lib.bsg_philox_invert_params(ctypes.byref(p._c()), y, ctypes.byref(x)), "philox_invert")
     return x.value
 
 
-def bijection_apply(variant: BijectionVariant, bits: int, seed: int, num_rounds: int, x: Any = None, *,
+class SplitMix64:  # splitmix.hpp:35-63
+    """Counter-based generator over the SplitMix64 stream: draw k of seed s is mix64(s + k * gamma)."""
+
+    GAMMA = 0x9E3779B97F4A7C15
+
+    def __init__(self, seed: int):
+        self.state = seed & 0xFFFFFFFFFFFFFFFF
+
+    def __call__(self) -> int:
+        self.state = (self.state + self.GAMMA) & 0xFFFFFFFFFFFFFFFF
+        return mix64(self.state)
+
+    @staticmethod
+    def min() -> int:
+        return 0
+
+    @staticmethod
+    def max() -> int:
+        return 0xFFFFFFFFFFFFFFFF
+
+    def below(self, bound: int) -> int:
+        """Unbiased draw from [0, bound) by rejection (splitmix.hpp:49-59)."""
+        if bound == 0:
+            raise InvalidArgument("bound must be >= 1")
+        full = 0xFFFFFFFFFFFFFFFF
+        limit = full - (full % bound)
+        while True:
+            v = self()
+            if v < limit:
+                return v % bound
+
+
+@dataclass
+class BijectionSpec:  # bijection.hpp:146-150
+    variant: Any = None  # LcgParams or VariablePhiloxParams
+    domain_bits: int = 0
+
+
+def make_bijection(p: Any) -> BijectionSpec:  # bijection.hpp:152-158
+    if isinstance(p, LcgParams):
+        return BijectionSpec(p, p.modulus_bits)
+    if isinstance(p, VariablePhiloxParams):
+        return BijectionSpec(p, p.total_bits)
+    raise InvalidArgument("make_bijection: LcgParams or VariablePhiloxParams expected")
+
+
+def bijection_spec_apply(spec: BijectionSpec, x: int) -> int:  # bijection.hpp:160-169
+    """bijection_apply(const BijectionSpec&, x) of the reference (the GPU batch form is bijection_apply)."""
+    if isinstance(spec.variant, LcgParams):
+        return lcg_apply(spec.variant, x)
+    return philox_apply(spec.variant, x)
+
+
+def bijection_apply(variant: Any, bits: int = 0, seed: int = 0, num_rounds: int = 24, x: Any = None, *,
                     start: int = 0, n: Optional[int] = None, inverse: bool = False, out: Any = None):
-    """GPU batch evaluation y[i] = f(x[i]) (or f^-1).  x=None evaluates counters start..start+n-1."""
+    """GPU batch evaluation y[i] = f(x[i]) (or f^-1).  x=None evaluates counters start..start+n-1.
+
+    Called as bijection_apply(spec, x) with a BijectionSpec and an integer x it is the reference's scalar
+    bijection_apply (bijection.hpp:160-169)."""
+    if isinstance(variant, BijectionSpec):
+        return bijection_spec_apply(variant, bits if x is None else x)
     if x is not None:
         xb = _Buf(x)
         if xb.itemsize != 8:
@@ -366,6 +432,19 @@ class Pipeline:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+def workspace_bytes() -> int:
+    """Device memory held by the library's cached workspaces on the current device (bsg_workspace_bytes)."""
+    b = ctypes.c_uint64()
+    check(lib.bsg_workspace_bytes(ctypes.byref(b)), "workspace_bytes")
+    return b.value
+
+
+def release_workspace() -> None:
+    """Free the cached workspaces of the current device (bsg_release_workspace); graphs captured from earlier
+    calls must not be replayed afterwards."""
+    check(lib.bsg_release_workspace(), "release_workspace")
 
 
 def kernel_launches() -> int:

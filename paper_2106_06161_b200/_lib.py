@@ -26,6 +26,12 @@ class bsg_shards(Structure):
     _fields_ = [("ptrs", c_void_p * 16), ("count", c_int32), ("reserved", c_int32), ("shard_elems", c_uint64)]
 
 
+class bsg_philox_params(Structure):
+    _fields_ = [("total_bits", c_int32), ("left_side_bits", c_int32), ("right_side_bits", c_int32),
+                ("num_rounds", c_int32), ("left_side_mask", c_uint64), ("right_side_mask", c_uint64),
+                ("round_keys", POINTER(c_uint32)), ("num_keys", c_uint64)]
+
+
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, POINTER(c_uint64), POINTER(c_uint64), c_void_p)
 
 # name -> (restype, argtypes); every symbol of include/bsg.h
@@ -38,6 +44,8 @@ SIGNATURES = {
     "bsg_lcg_apply": (c_int32, [c_int32, c_uint64, c_uint64, c_uint64, POINTER(c_uint64)]),
     "bsg_philox_apply": (c_int32, [c_int32, c_uint64, c_int32, c_uint64, POINTER(c_uint64)]),
     "bsg_philox_invert": (c_int32, [c_int32, c_uint64, c_int32, c_uint64, POINTER(c_uint64)]),
+    "bsg_philox_apply_params": (c_int32, [POINTER(bsg_philox_params), c_uint64, POINTER(c_uint64)]),
+    "bsg_philox_invert_params": (c_int32, [POINTER(bsg_philox_params), c_uint64, POINTER(c_uint64)]),
     "bsg_bijection_apply": (c_int32, [c_int32, c_int32, c_uint64, c_int32, c_int32, c_void_p, c_uint64, c_void_p,
                                       c_uint64, c_void_p]),
     "bsg_shuffle_indices": (c_int32, [c_uint64, POINTER(bsg_config), c_void_p, c_void_p]),
@@ -69,6 +77,7 @@ SIGNATURES = {
     "bsg_kernel_launches": (c_uint64, []),
     "bsg_set_force_compact": (c_int32, [c_int32]),
     "bsg_set_path": (c_int32, [c_int32]),
+    "bsg_workspace_bytes": (c_int32, [POINTER(c_uint64)]),
     "bsg_release_workspace": (c_int32, []),
 }
 

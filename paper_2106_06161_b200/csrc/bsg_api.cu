@@ -197,6 +197,19 @@ bsg_status ws_end(DeviceCtx* c, cudaStream_t s) {
   return BSG_OK;
 }
 
+// Sizes a workspace buffer for a call on stream s.  While s is being captured nothing may be allocated: the
+// buffer must already be large enough (one uncaptured call of the same shape), and it is marked captured so a
+// later larger uncaptured call retires it instead of freeing memory a graph still references.
+bsg_status ensure_ws(DevBuf& b, size_t n, cudaStream_t s) {
+  if (capturing(s)) {
+    if (!b.p || b.bytes < n) return fail(BSG_EINVAL, "graph capture: run this call once uncaptured first");
+    b.captured = true;
+    return BSG_OK;
+  }
+  BSG_CUDA(b.ensure(n));
+  return BSG_OK;
+}
+
 // Uploads the key schedule for generic-round Philox kernels.
 bsg_status upload_keys(DeviceCtx* c, BijParams& p, uint64_t seed, cudaStream_t s) {
   if (p.variant != bsg::kPhilox || p.rounds == 24) return BSG_OK;
@@ -334,7 +347,7 @@ bsg_status shuffle_device(DeviceCtx* c, const void* in, void* out, uint64_t m, u
   const int code = native_code(eb, in, out);
   if (code > 0) return run_range(c, m, cfg, 0, n, src, out, code, nullptr, s);
   // Other element sizes: permutation first, then a record gather.
-  BSG_CUDA(c->st_idx.ensure(m * 8));
+  BSG_TRY(ensure_ws(c->st_idx, m * 8, s));
   BSG_TRY(run_range(c, m, cfg, 0, n, bsg::Src{}, c->st_idx.p, 0, nullptr, s));
   BSG_TRY(ws_begin(c, s));
   BSG_CUDA(bsg::launch_gather_bytes(in, static_cast<const uint64_t*>(c->st_idx.p), out, m, eb, s));
@@ -405,6 +418,53 @@ bsg_status bsg_philox_invert(int32_t bits, uint64_t seed, int32_t rounds, uint64
   return BSG_OK;
 }
 
+// philox_apply / philox_invert over caller-held parameters (bijection.hpp:94-143), host scalar, 64-bit state as
+// in the reference so that any field combination it accepts gives its result.
+static bsg_status check_philox_params(const bsg_philox_params* p) {
+  if (!p) return fail(BSG_EINVAL, "null params");
+  if (p->left_side_bits < 0 || p->left_side_bits > 63 || p->right_side_bits < 0 || p->right_side_bits > 63 ||
+      p->right_side_bits < p->left_side_bits)
+    return fail(BSG_EINVAL, "side widths must satisfy 0 <= left_side_bits <= right_side_bits <= 63");
+  if (p->num_rounds > 0 && (!p->round_keys || p->num_keys < static_cast<uint64_t>(p->num_rounds)))
+    return fail(BSG_EINVAL, "round_keys holds fewer keys than num_rounds");
+  return BSG_OK;
+}
+
+bsg_status bsg_philox_apply_params(const bsg_philox_params* p, uint64_t x, uint64_t* y) {
+  BSG_TRY(check_philox_params(p));
+  if (p->total_bits < 64 && p->total_bits >= 0 && (x >> p->total_bits) != 0)
+    return fail(BSG_ERANGE, "philox_apply: x outside [0, 2^total_bits)");
+  const int L = p->left_side_bits, R = p->right_side_bits, d = R - L;
+  uint64_t a = x >> R, b = x & p->right_side_mask;
+  for (int i = 0; i < p->num_rounds; ++i) {
+    const uint64_t w = bsg::kM0 * a;  // 64-bit product: high word feeds the left side, low word the right
+    const uint64_t nb = ((w & 0xFFFFFFFFULL) << d) | (b >> L);
+    a = ((w >> 32) ^ p->round_keys[i] ^ b) & p->left_side_mask;
+    b = nb & p->right_side_mask;
+  }
+  *y = (a << R) | b;
+  return BSG_OK;
+}
+
+bsg_status bsg_philox_invert_params(const bsg_philox_params* p, uint64_t y, uint64_t* x) {
+  BSG_TRY(check_philox_params(p));
+  if (p->total_bits < 64 && p->total_bits >= 0 && (y >> p->total_bits) != 0)
+    return fail(BSG_ERANGE, "philox_invert: y outside [0, 2^total_bits)");
+  const int L = p->left_side_bits, R = p->right_side_bits, d = R - L;
+  uint64_t a = y >> R, b = y & p->right_side_mask;
+  for (int i = p->num_rounds - 1; i >= 0; --i) {
+    // b = (lo << d | spare) & right_mask with lo = M0 * prev_a mod 2^32: recover prev_a from lo mod 2^L through
+    // M0^-1, then the previous right side from the round's XOR (its top d bits are the spare bits)
+    const uint64_t prev_a = (bsg::kM0Inv * ((b >> d) & p->left_side_mask)) & p->left_side_mask;
+    const uint64_t hi = (bsg::kM0 * prev_a) >> 32;
+    const uint64_t prev_b = ((hi ^ p->round_keys[i] ^ a) & p->left_side_mask) | ((b & ((1ULL << d) - 1)) << L);
+    a = prev_a;
+    b = prev_b;
+  }
+  *x = (a << R) | b;
+  return BSG_OK;
+}
+
 bsg_status bsg_bijection_apply(int32_t variant, int32_t bits, uint64_t seed, int32_t rounds, int32_t inverse,
                                const uint64_t* x, uint64_t start, uint64_t* y, uint64_t n, void* stream) {
   BijParams p;
@@ -421,6 +481,8 @@ bsg_status bsg_bijection_apply(int32_t variant, int32_t bits, uint64_t seed, int
     }
     const uint64_t* dx = x;
     uint64_t* dy = y;
+    // staging buffers may still be read by an earlier asynchronous call of this context on another stream
+    BSG_TRY(ws_begin(c, s));
     if (x && !xd) {
       BSG_CUDA(c->st_in.ensure(n * 8));
       BSG_CUDA(cudaMemcpyAsync(c->st_in.p, x, n * 8, cudaMemcpyHostToDevice, s));
@@ -471,6 +533,7 @@ bsg_status bsg_shuffle_values(const void* in, void* out, uint64_t m, uint32_t el
     if (din && dout) return shuffle_device(c, in, out, m, elem_bytes, cfg, s);
     const void* di = in;
     void* dO = out;
+    BSG_TRY(ws_begin(c, s));  // order the staging writes after earlier asynchronous users of st_*
     if (!din) {
       BSG_CUDA(c->st_in.ensure(bytes));
       BSG_CUDA(cudaMemcpyAsync(c->st_in.p, in, bytes, cudaMemcpyHostToDevice, s));
@@ -506,6 +569,7 @@ bsg_status bsg_shuffle_values_batched(const void* in, void* out, uint64_t batch,
     const bool din = is_device_ptr(in), dout = is_device_ptr(out);
     const void* di = in;
     void* dO = out;
+    if (!din || !dout) BSG_TRY(ws_begin(c, s));  // staging writes after earlier asynchronous users of st_*
     if (!din) {
       BSG_CUDA(c->st_in.ensure(bytes));
       BSG_CUDA(cudaMemcpyAsync(c->st_in.p, in, bytes, cudaMemcpyHostToDevice, s));
@@ -555,6 +619,7 @@ bsg_status bsg_gather(const void* src, uint64_t src_len, const uint64_t* idx, vo
     const uint64_t* I = idx;
     void* O = out;
     const size_t sb = src_len * static_cast<size_t>(elem_bytes), ob = n * static_cast<size_t>(elem_bytes);
+    if (!ds || !di || !dout) BSG_TRY(ws_begin(c, s));  // staging writes after earlier asynchronous users of st_*
     if (!ds) {
       BSG_CUDA(c->st_in.ensure(sb));
       BSG_CUDA(cudaMemcpyAsync(c->st_in.p, src, sb, cudaMemcpyHostToDevice, s));
@@ -713,7 +778,7 @@ bsg_status bsg_route_by_dest(const void* in, uint64_t n_local, uint64_t global_o
     cudaStream_t s = as_stream(stream);
     if (!is_device_ptr(in) || !is_device_ptr(out_values) || !is_device_ptr(out_dest))
       return fail(BSG_EINVAL, "route_by_dest: device pointers only");
-    BSG_CUDA(c->st_idx.ensure(std::max<uint64_t>(n_local, 1) * 4 + 2 * 64 * 8));
+    BSG_TRY(ensure_ws(c->st_idx, std::max<uint64_t>(n_local, 1) * 4 + 2 * 64 * 8, s));
     char* w = static_cast<char*>(c->st_idx.p);
     bsg::RouteLaunch R;
     R.in = in;
@@ -760,6 +825,7 @@ bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uin
         (g_path == 2 || n * static_cast<uint64_t>(elem_bytes) >= g_partition_min_bytes) &&
         (capturing(s) ? (c->part.p && c->part.bytes >= bsg::partition_workspace_bytes(code, bits))
                       : c->part.ensure(bsg::partition_workspace_bytes(code, bits)) == cudaSuccess)) {
+      if (capturing(s)) c->part.captured = true;
       bsg::PartitionLaunch P;
       bsg::partition_layout(code, bits, false, c->part.p, P);
       P.in = values;
@@ -775,24 +841,70 @@ bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uin
   });
 }
 
+// Base of the allocation containing p (driver cuMemGetAddressRange through the runtime's entry-point query, so
+// libbsg does not link libcuda directly).
+static bsg_status alloc_base(const void* p, uintptr_t* base) {
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<GetRange>(f);
+  }();
+  if (!fn) return fail(BSG_ECUDA, "cuMemGetAddressRange unavailable");
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0) return fail(BSG_EINVAL, "not a device allocation");
+  *base = static_cast<uintptr_t>(b);
+  return BSG_OK;
+}
+
+static std::mutex g_ipc_mu;
+static std::vector<std::pair<void*, void*>> g_ipc_open;  // (returned pointer, mapped allocation base)
+
 bsg_status bsg_ipc_export(const void* dev_ptr, unsigned char handle_out[BSG_IPC_HANDLE_BYTES]) {
   cudaIpcMemHandle_t h;
-  BSG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
-  static_assert(sizeof(h) <= BSG_IPC_HANDLE_BYTES, "ipc handle size");
+  static_assert(sizeof(h) + 8 <= BSG_IPC_HANDLE_BYTES, "ipc handle size");
+  uintptr_t base = 0;
+  BSG_TRY(alloc_base(dev_ptr, &base));
+  BSG_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  const uint64_t off = reinterpret_cast<uintptr_t>(dev_ptr) - base;
   std::memset(handle_out, 0, BSG_IPC_HANDLE_BYTES);
   std::memcpy(handle_out, &h, sizeof(h));
+  std::memcpy(handle_out + sizeof(h), &off, 8);
   return BSG_OK;
 }
 
 bsg_status bsg_ipc_open(const unsigned char handle[BSG_IPC_HANDLE_BYTES], void** dev_ptr_out) {
   cudaIpcMemHandle_t h;
+  uint64_t off = 0;
   std::memcpy(&h, handle, sizeof(h));
-  BSG_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  std::memcpy(&off, handle + sizeof(h), 8);
+  void* base = nullptr;
+  BSG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr_out = static_cast<char*>(base) + off;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_open.emplace_back(*dev_ptr_out, base);
   return BSG_OK;
 }
 
 bsg_status bsg_ipc_close(void* dev_ptr) {
-  BSG_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (auto it = g_ipc_open.begin(); it != g_ipc_open.end(); ++it)
+      if (it->first == dev_ptr) {
+        base = it->second;
+        g_ipc_open.erase(it);
+        break;
+      }
+  }
+  if (!base) return fail(BSG_EINVAL, "ipc_close: pointer was not returned by bsg_ipc_open");
+  BSG_CUDA(cudaIpcCloseMemHandle(base));
   return BSG_OK;
 }
 
@@ -943,6 +1055,18 @@ int32_t bsg_set_force_compact(int32_t on) {
   const int old = g_force_compact;
   g_force_compact = on ? 1 : 0;
   return old;
+}
+
+bsg_status bsg_workspace_bytes(uint64_t* bytes) {
+  if (!bytes) return fail(BSG_EINVAL, "null pointer");
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    uint64_t t = 0;
+    for (const DevBuf* b : {&c->status, &c->scratch, &c->keys, &c->st_in, &c->st_out, &c->st_idx, &c->st_tmp,
+                            &c->part})
+      t += b->bytes;
+    *bytes = t;
+    return BSG_OK;
+  });
 }
 
 bsg_status bsg_release_workspace(void) {

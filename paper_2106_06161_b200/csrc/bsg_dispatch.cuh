@@ -26,13 +26,7 @@ cudaError_t run_shuffle(const ShuffleLaunch& a, cudaStream_t s) {
     constexpr uint64_t kTile = kThreads * kItems;
     const uint64_t grid = (len + kTile - 1) / kTile;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-#ifndef BSG_COMPACT_EARLY
-#define BSG_COMPACT_EARLY 0
-#endif
-    if constexpr (BSG_COMPACT_EARLY && sizeof(T) >= 4 && !std::is_same<T, IdxTag>::value) {
-      k_compact_early<KIND, CT, T, SH, kItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
-          a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
-    } else if constexpr (sizeof(T) >= 4 || std::is_same<T, IdxTag>::value) {
+    if constexpr (sizeof(T) >= 4 || std::is_same<T, IdxTag>::value) {
       k_compact_smem<KIND, CT, T, SH, kItems><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
           a.src, a.out, a.m, a.c0, a.c1, a.p, a.lb, a.count_out);
     } else {

@@ -441,85 +441,6 @@ __global__ void __launch_bounds__(kThreads) k_compact_smem(Src src, void* out_, 
 }
 
 
-// Early-issue variant: each survivor's payload is fetched into smem at its
-// COUNTER slot right after its image is known (loads interleave with the
-// cipher of the remaining items), then written out per (item, warp) run.
-template <int KIND, typename CT, typename T, bool SH, int ITEMS>
-__global__ void __launch_bounds__(kThreads) k_compact_early(Src src, void* out_, uint64_t m, uint64_t c0,
-                                                            uint64_t c1, BijParams p, Lookback lb,
-                                                            unsigned long long* count_out) {
-  constexpr int kTile = kThreads * ITEMS;
-  constexpr int kSlots = ITEMS * kWarps;
-  constexpr int kPerLane = kSlots / 32;
-  static_assert(kSlots % 32 == 0 && kPerLane <= 4, "slots");
-  __shared__ __align__(16) T s_val[kTile];
-  __shared__ uint32_t s_cnt[kSlots];
-  __shared__ unsigned long long s_prefix;
-  __shared__ uint32_t s_tile;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    const uint32_t t = atomicAdd(lb.tile_counter, 1u);
-    if (t == gridDim.x - 1) *lb.tile_counter = 0;
-    s_tile = t;
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t t0 = c0 + static_cast<uint64_t>(tile) * kTile + tid;
-  uint32_t mask[ITEMS];
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const uint64_t c = t0 + j * kThreads;
-    const CT y = bij<KIND, CT>(static_cast<CT>(c), p);
-    const bool keep = (c < c1) && (static_cast<uint64_t>(y) < m);
-    mask[j] = __ballot_sync(0xFFFFFFFFu, keep);
-    if (keep) cp_async_payload<T>(&s_val[j * kThreads + tid], src_addr<T, SH>(src, y));
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  if (lane == 0) {
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) s_cnt[j * kWarps + warp] = __popc(mask[j]);
-  }
-  __syncthreads();
-  uint32_t a[kPerLane], sum = 0;
-#pragma unroll
-  for (int i = 0; i < kPerLane; ++i) {
-    a[i] = s_cnt[lane * kPerLane + i];
-    sum += a[i];
-  }
-  uint32_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  uint32_t ex[kPerLane];
-  ex[0] = incl - sum;
-#pragma unroll
-  for (int i = 1; i < kPerLane; ++i) ex[i] = ex[i - 1] + a[i - 1];
-  if (warp == 0) {
-    const unsigned long long excl = lookback_warp(lb, tile, total);
-    if (lane == 0) s_prefix = excl;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
-  const unsigned long long prefix = s_prefix;
-  const uint32_t lt = lanemask_lt();
-  T* out = static_cast<T*>(out_) + prefix;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int e = j * kWarps + warp;
-    uint32_t base = 0;
-#pragma unroll
-    for (int i = 0; i < kPerLane; ++i) {
-      const uint32_t x = __shfl_sync(0xFFFFFFFFu, ex[i], e / kPerLane);
-      if (e % kPerLane == i) base = x;
-    }
-    if ((mask[j] >> lane) & 1u) st_out<T>(out + base + __popc(mask[j] & lt), s_val[j * kThreads + tid]);
-  }
-  if (count_out != nullptr && tile == gridDim.x - 1 && tid == 0) *count_out = prefix + total;
-}
-
 // --------------------------------------------------------------- batched path
 // Many independent shuffles of the same length m (BijectiveShuffleSampler,
 // stats.hpp:314-324: shuffle b is keyed by seed + b).  One CTA per shuffle:

@@ -648,8 +648,11 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   // keep the integer pipes busy (k_part1t: 5.16 vs 3.97 ms).
   // With 512 coarse buckets (domains of 2^30+) the 2-CTA TMA-fed form loses (C3-LCG P1 4.72 vs 4.05 ms).
   constexpr bool kTmaP1 = (KIND == kKindLcg || KIND == kKindDestArray) && sizeof(T) <= 8;
+  // cp.async.bulk needs 16-byte aligned global addresses: a caller's array that is only element-aligned (e.g. the
+  // view x[1:] of a u64 tensor) takes the register-loading k_part1.
+  const bool in_aligned = (reinterpret_cast<uintptr_t>(a.in) & 15u) == 0;
   uint64_t done1 = 0;
-  if (kTmaP1 && full1 > 0 && nb1 <= 256) {
+  if (kTmaP1 && in_aligned && full1 > 0 && nb1 <= 256) {
     const size_t smt = kP1Tile * (2 * sizeof(T) + 4);
     cudaFuncSetAttribute(k_part1t<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
     int per = 1;

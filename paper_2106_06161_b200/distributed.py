@@ -77,10 +77,11 @@ def _gpu_range(m: int, cfg: ShuffleConfig, begin: int, end: int, values, out, sh
 
 
 def shuffle_values(values, m: int, cfg: Optional[ShuffleConfig] = None, group=None, out=None, shards=None,
-                   range_fn: Optional[Callable] = None):
+                   range_fn: Optional[Callable] = None, dtype=None):
     """Distributed shuffle of m elements.
 
-    values: the full input replicated on this rank (or None with `shards` from `ipc_shards`).
+    values: the full input replicated on this rank (or None with `shards`, the `.table` of `ipc_shards`, in which
+    case `out` or `dtype` gives the element type).
     Returns (piece, global_offset, counts): piece[:counts[rank]] are global output positions
     [global_offset, global_offset + counts[rank]).
     `range_fn(m, cfg, begin, end, values, out) -> count` replaces the GPU kernel (tests inject the oracle).
@@ -94,7 +95,7 @@ def shuffle_values(values, m: int, cfg: Optional[ShuffleConfig] = None, group=No
     begin, end = counter_range(m, rank, world)
     if out is None:
         like = values if values is not None else None
-        dtype = like.dtype if like is not None else torch.int64
+        dtype = like.dtype if like is not None else (dtype or torch.int64)
         device = like.device if like is not None else torch.device("cuda", torch.cuda.current_device())
         out = torch.empty(end - begin, dtype=dtype, device=device)
     fn = range_fn or (lambda *a: _gpu_range(*a, shards=shards))
@@ -172,26 +173,57 @@ def shuffle_values_sharded(local_shard, m: int, cfg: Optional[ShuffleConfig] = N
     return (scatter_fn or _gpu_scatter)(rv, rd, S)
 
 
-def ipc_shards(local_shard, group=None) -> "_lib.bsg_shards":
+IPC_HANDLE_BYTES = 80  # BSG_IPC_HANDLE_BYTES: CUDA IPC handle of the allocation + offset of the shard in it
+
+
+class IpcShards:
+    """The bsg_shards table of a sharded input (every rank's shard mapped into this process) and the peer
+    mappings behind it; `close()` (or a with-block) unmaps them."""
+
+    def __init__(self, table, opened):
+        self.table = table
+        self._opened = opened
+
+    def close(self):
+        while self._opened:
+            check(lib.bsg_ipc_close(self._opened.pop()), "ipc_close")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def ipc_shards(local_shard, group=None) -> IpcShards:
     """Exchange CUDA IPC handles of each rank's equally sized input shard and map every peer's shard
-    (NVLink peer reads).  Returns the bsg_shards table for `shuffle_values(..., shards=...)`."""
+    (NVLink peer reads).  Handles carry the shard's offset inside its allocation, so tensors from PyTorch's
+    caching allocator map correctly.  Returns an IpcShards whose `.table` is the bsg_shards table for
+    `shuffle_values(..., shards=...)`; close it when done."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    h = (ctypes.c_ubyte * 64)()
+    h = (ctypes.c_ubyte * IPC_HANDLE_BYTES)()
     check(lib.bsg_ipc_export(local_shard.data_ptr(), h), "ipc_export")
     handles = [None] * world
     dist.all_gather_object(handles, (bytes(h), local_shard.numel()), group=group)
-    tab = _lib.bsg_shards()
     sizes = {n for _, n in handles}
     if len(sizes) != 1:
         raise _lib.InvalidArgument("input shards must be equally sized")
-    for g, (hb, _) in enumerate(handles):
-        if g == rank:
-            tab.ptrs[g] = local_shard.data_ptr()
-            continue
-        p = ctypes.c_void_p()
-        check(lib.bsg_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(hb), ctypes.byref(p)), "ipc_open")
-        tab.ptrs[g] = p.value
+    tab = _lib.bsg_shards()
+    opened = []
+    try:
+        for g, (hb, _) in enumerate(handles):
+            if g == rank:
+                tab.ptrs[g] = local_shard.data_ptr()
+                continue
+            p = ctypes.c_void_p()
+            check(lib.bsg_ipc_open((ctypes.c_ubyte * IPC_HANDLE_BYTES).from_buffer_copy(hb), ctypes.byref(p)),
+                  "ipc_open")
+            opened.append(p.value)
+            tab.ptrs[g] = p.value
+    except BaseException:
+        IpcShards(tab, opened).close()
+        raise
     tab.count = world
     tab.shard_elems = sizes.pop()
-    return tab
+    return IpcShards(tab, opened)

@@ -78,3 +78,75 @@ def test_two_ranks_on_one_gpu(orc):
     m = 1 << 20
     exp = orc.shuffle_values(np.arange(m, dtype=np.uint64) * 7, 5, 1, 24)
     assert np.array_equal(np.concatenate([out[r][("sharded", m)] for r in range(world)]).view(np.uint64), exp)
+
+
+def _ipc_worker(rank, world, port, q):
+    """Sharded input with real CUDA IPC: each rank owns one shard placed at an offset inside a larger torch
+    allocation (the case the round-1 handle exchange got wrong), maps every peer's shard with ipc_shards and
+    shuffles its counter range through the shard table (payload reads through the peer mappings)."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_06161_b200 as bsg
+    from paper_2106_06161_b200 import distributed as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for m, variant, eb in (((1 << 21), 1, 8), ((1 << 21) + 11, 1, 8), ((1 << 20) + 3, 0, 16), ((1 << 21), 1, 16)):
+            S = (m + world - 1) // world
+            lo = rank * S
+            if eb == 8:
+                big = torch.empty(S + 4096, dtype=torch.int64, device="cuda")
+                local = big[4096:]  # 32 KiB into the allocation
+                local.copy_(torch.arange(lo, lo + S, dtype=torch.int64, device="cuda") * 3 + 1)
+                dtype = torch.int64
+            else:
+                big = torch.empty((S + 256, 2), dtype=torch.int64, device="cuda")
+                local = big[256:]
+                idx = torch.arange(lo, lo + S, dtype=torch.int64, device="cuda")
+                local[:, 0] = idx
+                local[:, 1] = idx * 7 + 5
+                local = local.view(torch.complex128).view(-1)
+                dtype = torch.complex128
+            torch.cuda.synchronize()
+            dist.barrier()
+            with D.ipc_shards(local) as ipc:
+                piece, off, counts = D.shuffle_values(None, m, bsg.ShuffleConfig(seed=m, variant=bsg.BijectionVariant(
+                    variant)), shards=ipc.table, dtype=dtype)
+                torch.cuda.synchronize()
+                dist.barrier()  # peers keep reading this rank's shard until every rank is done
+            res[(m, variant, eb)] = (off, piece[:counts[rank]].view(torch.int64).cpu().numpy().copy())
+            del big, local
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_sharded_ranks_on_one_gpu(orc, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for m, variant, eb in (((1 << 21), 1, 8), ((1 << 21) + 11, 1, 8), ((1 << 20) + 3, 0, 16), ((1 << 21), 1, 16)):
+        perm = orc.shuffle_indices(m, m, variant, 24)
+        if eb == 8:
+            exp = perm * np.uint64(3) + np.uint64(1)
+        else:
+            exp = np.stack([perm, perm * np.uint64(7) + np.uint64(5)], axis=1).reshape(-1)
+        full = np.empty(m * (eb // 8), dtype=np.uint64)
+        k = eb // 8
+        for r in range(world):
+            off, piece = out[r][(m, variant, eb)]
+            full[off * k:off * k + len(piece)] = piece.view(np.uint64)
+        assert np.array_equal(full, exp), (world, m, variant, eb)

@@ -77,3 +77,45 @@ def test_transfer_plan_moves_only_boundaries():
     moved = sum(plan[s][d] for s in range(world) for d in range(world) if s != d)
     assert moved == 10 + 5  # only the boundary slack crosses ranks
     assert D.offsets_from_counts(counts, 2) == 500
+
+
+def test_philox_params_path_matches_reference_kats(golden):
+    """philox_apply/philox_invert over caller-held params (bsg_philox_*_params) reproduce every reference KAT
+    (widths 2..63, rounds 3..100) -- the path the C++ shim and this mirror use."""
+    cache = {}
+    for bits, seed, rounds, x, y in golden["philox_apply"]:
+        p = cache.setdefault((bits, seed, rounds), bsg.make_philox(bits, seed, rounds))
+        assert bsg.philox_apply(p, x) == y
+    for bits, seed, rounds, y, x in golden["philox_invert"]:
+        p = cache.setdefault((bits, seed, rounds), bsg.make_philox(bits, seed, rounds))
+        assert bsg.philox_invert(p, y) == x
+
+
+def test_caller_built_philox_params():  # unit_bijection.cpp:106-115, 138-147
+    p = bsg.VariablePhiloxParams(total_bits=8, left_side_bits=4, right_side_bits=4, num_rounds=0,
+                                 left_side_mask=0xF, right_side_mask=0xF)
+    assert bsg.philox_apply(p, 0b10110011) == 0b10110011
+    q = bsg.VariablePhiloxParams(6, 3, 3, 0, 0x7, 0x7)
+    assert bsg.philox_invert(q, 0b101101) == 0b101101
+    r = bsg.make_philox(20, 99)
+    y = bsg.philox_apply(r, 12345)
+    r.round_keys[3] ^= 1
+    y2 = bsg.philox_apply(r, 12345)
+    assert y2 != y and bsg.philox_invert(r, y2) == 12345
+    r.num_rounds = 40  # more rounds than keys
+    with pytest.raises(bsg.InvalidArgument):
+        bsg.philox_apply(r, 1)
+
+
+def test_bijection_spec_and_splitmix():  # bijection.hpp:146-169, splitmix.hpp:35-63
+    lcg = bsg.make_bijection(bsg.LcgParams(4, 1, 0))
+    assert lcg.domain_bits == 4 and bsg.bijection_apply(lcg, 9) == 9
+    with pytest.raises(bsg.OutOfRange):
+        bsg.bijection_apply(lcg, 16)
+    ph = bsg.make_bijection(bsg.make_philox(8, 7))
+    assert ph.domain_bits == 8 and sorted(bsg.bijection_apply(ph, x) for x in range(256)) == list(range(256))
+    g = bsg.SplitMix64(777)
+    assert g() == bsg.mix64((777 + 0x9E3779B97F4A7C15) & (2**64 - 1))
+    assert all(g.below(7) < 7 for _ in range(100))
+    with pytest.raises(bsg.InvalidArgument):
+        g.below(0)

@@ -722,3 +722,86 @@ def test_partitioned_random_shapes(bsg, cuda):
             assert np.array_equal(got, O.shuffle_indices(m, seed, variant, rounds)), (m, seed, variant, rounds, dt)
     finally:
         bsg.set_path(old)
+
+
+def test_c5_kernel_sharded_16byte_wide_counters(bsg, cuda):
+    """The C5 per-rank kernel: m = 2^33 16-byte {key, value} records read through an 8-entry shard table
+    (k_pow2 with 64-bit counters, uint4 payload, sharded source), on counter slices of three ranks' ranges.
+    The 8 shards of 2^30 records alias two 16 GiB buffers A/B (shard g -> A if g even), so the record read
+    for image j is {key = j mod 2^30, value = tag(j >> 30)}: both the in-shard index and the shard choice are
+    checked against the oracle's images."""
+    from paper_2106_06161_b200 import _lib
+    m, S, G = 1 << 33, 1 << 30, 8
+    tags = (0xAAAA0000, 0xBBBB0000)
+    bufs = []
+    for t in tags:
+        rec = cuda.empty((S, 2), dtype=cuda.int64, device="cuda")
+        rec[:, 0] = cuda.arange(S, dtype=cuda.int64, device="cuda")
+        rec[:, 1] = t
+        bufs.append(rec)
+    sh = _lib.bsg_shards()
+    for g in range(G):
+        sh.ptrs[g] = bufs[g & 1].data_ptr()
+    sh.count, sh.shard_elems = G, S
+    try:
+        for variant in (PHILOX, LCG):
+            cfg = cfg_of(bsg, seed=0x5EED, variant=variant)._c()
+            for a, b in ((0, 1 << 16), ((3 << 30) - 7000, (3 << 30) + 9000), (m - 4096, m)):
+                exp = O.shuffle_indices_range(m, 0x5EED, variant, 24, a, b)
+                out = cuda.empty((b - a, 2), dtype=cuda.int64, device="cuda")
+                cnt = ctypes.c_uint64()
+                _lib.check(_lib.lib.bsg_shuffle_range(m, ctypes.byref(cfg), a, b, None, ctypes.byref(sh),
+                                                      out.data_ptr(), 16, ctypes.addressof(cnt), None), "c5 range")
+                assert cnt.value == b - a
+                got = out.cpu().numpy().view(np.uint64)
+                assert np.array_equal(got[:, 0], exp & np.uint64(S - 1)), (variant, a)
+                assert np.array_equal(got[:, 1], np.where((exp >> np.uint64(30)) & np.uint64(1), np.uint64(tags[1]),
+                                                          np.uint64(tags[0]))), (variant, a)
+    finally:
+        del bufs
+        cuda.cuda.empty_cache()
+
+
+def test_partition_path_unaligned_input(bsg, cuda):
+    """an element-aligned but not 16-byte-aligned input (the view x[1:]) on the partitioned path with
+    the LCG (whose P1 is TMA-fed when the input is aligned) must not fault and must match the oracle."""
+    for m, path in (((1 << 25), 0), ((1 << 20), 2), ((1 << 20) + 3, 2)):
+        base = cuda.arange(m + 1, dtype=cuda.int64, device="cuda")
+        x = base[1:]
+        assert x.data_ptr() % 16 == 8
+        old = bsg.set_path(path)
+        try:
+            out = bsg.shuffle_values(x, cfg_of(bsg, seed=77, variant=LCG))
+        finally:
+            bsg.set_path(old)
+        exp = O.shuffle_indices(m, 77, LCG, 24) + np.uint64(1)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), exp), (m, path)
+    # the scatter-by-permutation entry point takes the same TMA-fed P1 for its values
+    from paper_2106_06161_b200 import _lib
+    n = 1 << 20
+    vals = cuda.arange(n + 1, dtype=cuda.int64, device="cuda")[1:]
+    dest = cuda.from_numpy(O.shuffle_indices(n, 5).astype(np.int64)).to("cuda").to(cuda.int32)
+    out = cuda.empty(n, dtype=cuda.int64, device="cuda")
+    old = bsg.set_path(2)
+    try:
+        _lib.check(_lib.lib.bsg_scatter_permutation(vals.data_ptr(), dest.data_ptr(), n, out.data_ptr(), 8, None),
+                   "scatter")
+    finally:
+        bsg.set_path(old)
+    exp = np.empty(n, dtype=np.uint64)
+    exp[O.shuffle_indices(n, 5)] = np.arange(1, n + 1, dtype=np.uint64)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), exp)
+
+
+def test_workspace_bytes_and_release(bsg, cuda):
+    vals = cuda.arange(1 << 20, dtype=cuda.int64, device="cuda")
+    old = bsg.set_path(2)
+    try:
+        bsg.shuffle_values(vals, cfg_of(bsg, seed=1))
+    finally:
+        bsg.set_path(old)
+    cuda.cuda.synchronize()
+    held = bsg.workspace_bytes()
+    assert held >= (1 << 20) * 14
+    bsg.release_workspace()
+    assert bsg.workspace_bytes() < held
