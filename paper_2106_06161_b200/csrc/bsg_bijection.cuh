@@ -91,6 +91,9 @@ struct BijParams {
   // Top-aligned inverse (philox_inv_top): shift 32 - L, M0^-1 << (32 - L), keys << (32 - L).
   uint32_t sh = 0, inv_top = 0;
   uint32_t ktop[kParamKeys] = {};
+  // High product on the FP64 pipe (philox_inv_top): fma_rd(2^52 + X, hc, hk) = 1.5 * 2^52 + floor(X * M0' / 2^32)
+  // exactly, M0' = M0 mod 2^(32+L); hc = M0' / 2^32, hk = 1.5 * 2^52 - M0' * 2^20.  Valid for L <= 16.
+  double hc = 0.0, hk = 0.0;
 };
 
 // ---------------------------------------------------------------------------
@@ -176,15 +179,33 @@ BSG_HD uint64_t philox_fwd(uint64_t x, const BijParams& p) {
 //       the next round needs lo = (x >> 1) | sp << (L-1): one funnel shift of
 //       (Z:Y) with Z = the previous x (bit 0 = sp), and Z' = Y >> sh = x.
 // No masks are needed anywhere inside the loop.
+//
+// The high word HW = umulhi(X, M0lo) + X * M0hi (IMAD.HI + IMAD, 6 of the 8
+// FMA-heavy cycles of a round) is computed on the FP64 pipe instead: with
+// M0' = M0 mod 2^(32+L), HW == floor(X * M0' / 2^32) (mod 2^32) because
+// X * (M0hi - M0' div 2^32) is a multiple of 2^L * 2^(32-L).  A round-down
+// DFMA of the biased double 2^52 + X (bit pattern {X, 0x43300000}) by
+// hc = M0' / 2^32 plus hk = 1.5 * 2^52 - M0' * 2^20 evaluates
+// X * M0' / 2^32 + 1.5 * 2^52 exactly before its single rounding (every
+// operand is exact in 53 bits for L <= 16), so the result's low word is that
+// floor: one DFMA replaces IMAD.HI + IMAD, bit-exact for every width
+// (tools/microbench/mb9.cu checks all widths 2..32; 2^29 ciphers 3.50 -> 2.89
+// ms, 2^30 with L = R 6.42 -> 4.68 ms on B200).
 #ifdef __CUDACC__
-template <int D, int NR>
+__device__ __forceinline__ uint32_t inv_high_word(uint32_t X, const BijParams& p) {
+  return static_cast<uint32_t>(__double2loint(__fma_rd(__hiloint2double(0x43300000, static_cast<int>(X)), p.hc, p.hk)));
+}
+
+// F64: the high word on the FP64 pipe (needs L <= 16, i.e. bits <= 33; the partitioned kernels' domains);
+// otherwise IMAD.HI + IMAD.
+template <int D, int NR, bool F64 = true>
 __device__ __forceinline__ uint64_t philox_inv_top(uint64_t y, const BijParams& p) {
   const uint32_t sh = p.sh;
   const uint32_t t0 = static_cast<uint32_t>(y >> p.R), t1 = static_cast<uint32_t>(y) & p.RM;
   uint32_t A = t0 << sh, B = D ? (t1 >> 1) : t1, Z = t1;
   auto round = [&](uint32_t ktop) {
     const uint32_t X = B * p.inv_top;
-    const uint32_t hw = __umulhi(X, kM0Lo) + X * kM0Hi;
+    const uint32_t hw = F64 ? inv_high_word(X, p) : __umulhi(X, kM0Lo) + X * kM0Hi;
     const uint32_t Y = hw ^ ktop ^ A;
     if (D) {
       B = __funnelshift_rc(Y, Z, sh + 1);  // (Y >> (sh+1)) | (Z << (L-1)); L == 1 clamps to Z
@@ -209,7 +230,7 @@ __device__ __forceinline__ uint64_t philox_inv_top(uint64_t y, const BijParams& 
 template <int D, int NR>
 BSG_HD uint64_t philox_inv(uint64_t y, const BijParams& p) {
 #ifdef __CUDA_ARCH__
-  return philox_inv_top<D, NR>(y, p);
+  return p.L <= 16 ? philox_inv_top<D, NR, true>(y, p) : philox_inv_top<D, NR, false>(y, p);
 #else  // host: the reference's round form (bijection.hpp:127-141)
   uint32_t t0 = static_cast<uint32_t>(y >> p.R);
   uint32_t t1 = static_cast<uint32_t>(y) & p.RM;
@@ -268,6 +289,11 @@ inline int make_params(int variant, int bits, uint64_t seed, int rounds, BijPara
   p.rounds = rounds;
   p.sh = static_cast<uint32_t>(32 - p.L);
   p.inv_top = kM0InvLo << p.sh;
+  if (p.L <= 16) {
+    const uint64_t m0p = kM0 & ((1ULL << (32 + p.L)) - 1);
+    p.hc = static_cast<double>(m0p) * 0x1p-32;
+    p.hk = 0x1.8p52 - static_cast<double>(m0p) * 0x1p20;
+  }
   for (int i = 0; i < rounds && i < kParamKeys; ++i) {
     p.keys[i] = round_key(seed, i);
     p.ktop[i] = p.keys[i] << p.sh;

@@ -41,9 +41,27 @@ namespace {
 #ifndef BSG_P1_THREADS
 #define BSG_P1_THREADS 256
 #endif
+// P1 occupancy and where the inverse cipher's high product runs, per split: D = R - L (1 for odd widths, C2).
+// Measured on B200 (tools/ktime.py, 2^29 u64): D = 1 with the high product on the FP64 pipe at 2 CTAs/SM
+// (104 registers) 3.67 ms against 3.97 ms for IMAD.HI at 3 CTAs/SM; D = 0 (C3) stays on IMAD.HI at 3 CTAs/SM
+// (4.06 ms; the FP64 form there loses a CTA per SM and measured 4.47-4.58 ms).
 #ifndef BSG_P1_MINB
 #define BSG_P1_MINB 3
 #endif
+#ifndef BSG_P1_MINB_F64
+#define BSG_P1_MINB_F64 2
+#endif
+#ifndef BSG_P1_F64
+#define BSG_P1_F64 1  // D = 1 only
+#endif
+#ifndef BSG_P1_F64_D0
+#define BSG_P1_F64_D0 0
+#endif
+template <int KIND, int D>
+constexpr bool p1_f64() {
+  return (KIND == kKindPh0 || KIND == kKindPh1 || KIND == kKindPh0G || KIND == kKindPh1G) &&
+         (D ? BSG_P1_F64 != 0 : BSG_P1_F64_D0 != 0);
+}
 #ifndef BSG_P2_THREADS
 #define BSG_P2_THREADS 256
 #endif
@@ -64,8 +82,9 @@ constexpr int kKindDestArray = 100;  // destinations come from an array (scatter
 template <int KIND, int D>
 __device__ __forceinline__ uint32_t inv_bij(uint32_t y, const BijParams& p) {
   if constexpr (KIND == kKindLcg) return static_cast<uint32_t>(lcg_inv(y, p));
-  else if constexpr (KIND == kKindPh0 || KIND == kKindPh1) return static_cast<uint32_t>(philox_inv<D, 24>(y, p));
-  else return static_cast<uint32_t>(philox_inv<D, 0>(y, p));
+  // partitioned domains have bits <= 32 (L <= 16): the high product runs on the FP64 pipe
+  else if constexpr (KIND == kKindPh0 || KIND == kKindPh1) return static_cast<uint32_t>(philox_inv_top<D, 24, p1_f64<KIND, D>()>(y, p));
+  else return static_cast<uint32_t>(philox_inv_top<D, 0, p1_f64<KIND, D>()>(y, p));
 }
 
 // Block-wide exclusive scan of `nb` <= 2 * blockDim.x bin counts.
@@ -142,7 +161,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // PAD: non-power-of-two domain, only inputs j < mv exist (the last tile may be partial); tile0 offsets the
 // tiles of a launch (the partial tail after k_part1t's full tiles).
 template <int KIND, int D, typename T, bool PAD = false>
-__global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2)
+__global__ void __launch_bounds__(kP1Threads, sizeof(T) > 8 ? 2 : (p1_f64<KIND, D>() ? BSG_P1_MINB_F64 : BSG_P1_MINB))
     k_part1(const T* __restrict__ in, T* __restrict__ tv, uint32_t* __restrict__ td, uint32_t* __restrict__ cur1,
             BijParams p, int bshift, int nb, uint64_t w1, const uint32_t* __restrict__ dsrc, uint64_t mv = 0,
             uint32_t tile0 = 0) {
@@ -178,14 +197,14 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) <= 8 ? BSG_P1_MINB : 2)
     if (valid(i)) rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
   }
   __syncthreads();
-  scan_bins(hist, start, nb, wt);
-  // Cursor atomics (nb <= 2 * blockDim) are issued first and consumed after the scatter (latency hidden).
+  // Cursor atomics (nb <= 2 * blockDim) are issued before the scan and consumed after the scatter (latency hidden).
   uint32_t g[2] = {0u, 0u};
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = tid + k * kP1Threads;
-    if (i < nb) g[k] = atomicAdd(cur1 + i, hist[i]);
+    if (i < nb && hist[i]) g[k] = atomicAdd(cur1 + i, hist[i]);
   }
+  scan_bins(hist, start, nb, wt);
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
 #pragma unroll
@@ -250,13 +269,13 @@ __global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in,
       rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
     }
     __syncthreads();
-    scan_bins(hist, start, nb, wt);
     uint32_t g[2] = {0u, 0u};
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int i = tid + k * kP1Threads;
-      if (i < nb) g[k] = atomicAdd(cur1 + i, hist[i]);
+      if (i < nb && hist[i]) g[k] = atomicAdd(cur1 + i, hist[i]);
     }
+    scan_bins(hist, start, nb, wt);
 #pragma unroll
     for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
     mbar_wait(&bar, phase);  // this tile's values have landed
@@ -379,10 +398,12 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     bulk_g2s(gv, tv + e0, kP2Tile * sizeof(T), &bar);
     bulk_g2s(gd, td + e0, kP2Tile * 4, &bar);
   };
-  const uint32_t tpb = static_cast<uint32_t>(w1 / kP2Tile);  // tile slots per coarse bucket
-  auto fill = [&](uint32_t t) -> uint32_t {                   // valid elements of tile t (0: empty)
+  // w1 (coarse bucket capacity) is a power of two >= kP2Tile: shifts, not 64-bit divisions
+  const int w1log = 63 - __clzll(static_cast<long long>(w1));
+  const int tpblog = w1log - kP2TileLog;  // log2(tile slots per coarse bucket)
+  auto fill = [&](uint32_t t) -> uint32_t {  // valid elements of tile t (0: empty)
     if (!cnt1) return kP2Tile;
-    const uint32_t c = cnt1[t / tpb], k0 = (t % tpb) * kP2Tile;
+    const uint32_t c = cnt1[t >> tpblog], k0 = (t & ((1u << tpblog) - 1)) * kP2Tile;
     return c > k0 ? min(c - k0, static_cast<uint32_t>(kP2Tile)) : 0u;
   };
   auto next = [&](uint32_t t) {
@@ -395,8 +416,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
   for (; t < ntiles; phase ^= 1) {
     mbar_wait(&bar, phase);
     const uint32_t nv = fill(t), tn = next(t + gridDim.x);
-    const uint64_t t0 = static_cast<uint64_t>(t) * kP2Tile;
-    const uint64_t coarse = t0 / w1;
+    const uint64_t coarse = t >> tpblog;
     uint32_t d[kP2Items], rk[kP2Items];
 #ifndef BSG_P2T_EARLY
 #define BSG_P2T_EARLY 1
@@ -420,16 +440,17 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     for (int i = 0; i < kP2Items; ++i)
       if (tid + i * kP2Threads < static_cast<int>(nv)) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
     __syncthreads();
-    scan_bins(hist, start, nb2, wt);
+    // The window-cursor atomics (global, one per window with elements) are issued before the scan and consumed
+    // after the scatter, so their L2 round trip overlaps both (it was 9% of P2's stall samples when consumed
+    // right away).
     uint32_t* cur = cur2 + coarse * nb2;
-    const uint64_t win0 = coarse * w1;
-    if (tid < nb2)
-      delta[tid] = static_cast<uint32_t>(win0 + (static_cast<uint64_t>(tid) << w2)) + atomicAdd(cur + tid, hist[tid]) -
-                   start[tid];
-    if (tid + kP2Threads < nb2) {
-      const int q = tid + kP2Threads;
-      delta[q] = static_cast<uint32_t>(win0 + (static_cast<uint64_t>(q) << w2)) + atomicAdd(cur + q, hist[q]) - start[q];
+    uint32_t g[2] = {0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * kP2Threads;
+      if (q < nb2 && hist[q]) g[k] = atomicAdd(cur + q, hist[q]);
     }
+    scan_bins(hist, start, nb2, wt);
 #pragma unroll
     for (int i = 0; i < kP2Items; ++i) {
       if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
@@ -437,6 +458,12 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
       if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
       else sv[s] = gv[tid + i * kP2Threads];
       sd[s] = d[i];
+    }
+    const uint32_t win0 = static_cast<uint32_t>(coarse << w1log);  // positions fit 32 bits (bits <= 32)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * kP2Threads;
+      if (q < nb2) delta[q] = win0 + (static_cast<uint32_t>(q) << w2) + g[k] - start[q];
     }
     __syncthreads();  // staging consumed, sorted tile complete, delta ready
     if (tid < nb2) hist[tid] = 0;
