@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-comparators", action="store_true", help="skip gather-bound / CUB sort-shuffle timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(steps, 5))")
+    ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)  # internal: the CPU baseline leg
     return ap.parse_args()
 
 
@@ -148,14 +149,12 @@ def reference_arm(args, rank, world):
     per = (ctypes.c_double * calls)()
     fnv = ctypes.c_uint64()
     if batch:
-        # BijectiveShuffleSampler-style: seed + b, one reference call per shuffle (u64 payload path).
-        t_all = []
-        for _ in range(calls):
-            t0 = time.perf_counter()
-            for b in range(batch):
-                O.REF.ref_shuffle_indices(m, SEED + b, variant, 24, 0, _scratch(m))
-            t_all.append(time.perf_counter() - t0)
-        times = t_all[args.warmup:]
+        # BijectiveShuffleSampler convention (seed + b, stats.hpp:314-324): one shuffle_values_into call per u32 row,
+        # rows spread over all host threads.
+        note = f"{batch} shuffle_values_into calls on iota({m}) u32 rows (seed + b) over all host threads"
+        rc = O.REF.ref_time_batched_u32_calls(batch, m, SEED, variant, 24, 0, calls, per)
+        assert rc == 0, rc
+        times = list(per)[args.warmup:]
         bytes_step = 2 * batch * m * eb
     elif eb == 16:
         m_sample = min(m, 1 << 28)
@@ -181,51 +180,82 @@ def reference_arm(args, rank, world):
                    "seed": SEED, "rounds": 24, "variant": "VariablePhilox" if variant else "Lcg"},
         "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": f"n={m_sample} {DTYPES[eb]} per step ({note}); {os.path.basename(O.REF.path)}, "
-                                   f"avx512={bool(O.REF.ref_avx512_active())}, workers=0 (all host threads)"},
+                                   f"avx512={bool(O.REF.ref_avx512_active())}, workers=0 (all host threads), "
+                                   f"host CPU: {cpu_model()}"},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-_SCR = {}
-
-
-def _scratch(m):
-    import numpy as np
-    if m not in _SCR:
-        _SCR[m] = np.empty(m, dtype=np.uint64)
-    return _SCR[m].ctypes.data
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline_leg(args, cfgname):
-    """Reference CPU shuffle on this host, bounded sample (rank 0, N=1)."""
+    """Reference CPU shuffle on this host, bounded sample (rank 0, N=1; run in its own process by main())."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ctypes
+
     import oracle as O
     if O.REF is None:
         return None
     m, eb, variant, batch, desc = CONFIGS[cfgname]
-    if batch:
-        return None
+    cores = int(O.REF.ref_hardware_threads())
+    lib = f"{os.path.basename(O.REF.path)}, avx512={bool(O.REF.ref_avx512_active())}, host CPU: {cpu_model()}"
     trials = 3 if m >= (1 << 26) else 5
+    per = (ctypes.c_double * (trials + 1))()
+    if batch:
+        assert O.REF.ref_time_batched_u32_calls(batch, m, SEED, variant, 24, 0, trials + 1, per) == 0
+        mean = sum(list(per)[1:]) / trials
+        return {"value": round(2 * batch * m * eb / mean / 1e9, 3), "unit": "GB/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"the full per-GPU workload: {batch} shuffle_values_into calls on iota({m}) u32 rows, seed+b "
+                          f"(BijectiveShuffleSampler, stats.hpp:314-324), rows spread over {cores} threads; "
+                          f"1 warm-up + mean of {trials}; {lib}"}
     if eb == 16:
-        import ctypes
         ms = min(m, 1 << 28)
-        per = (ctypes.c_double * (trials + 1))()
         assert O.REF.ref_time_shuffle_pairs_calls(ms, SEED, variant, 24, 0, trials + 1, per) == 0
         mean = sum(list(per)[1:]) / trials
-        return {"value": round(2 * ms * 16 / mean / 1e9, 3), "unit": "GB/s",
-                "cores": int(O.REF.ref_hardware_threads()), "kind": "reference",
-                "sample": f"n={ms} 16-byte records (bench.hpp:112-114 Pair), 1 warm-up + mean of {trials}, "
-                          f"{os.path.basename(O.REF.path)}, avx512={bool(O.REF.ref_avx512_active())}"}
+        return {"value": round(2 * ms * 16 / mean / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+                "sample": f"n={ms} 16-byte records (bench.hpp:112-114 Pair), 1 warm-up + mean of {trials}, {lib}"}
     mean, _ = O.ref_time_shuffle_u64(m, SEED, variant, 24, trials)
-    return {"value": round(2 * m * 8 / mean / 1e9, 3), "unit": "GB/s", "cores": int(O.REF.ref_hardware_threads()),
-            "kind": "reference",
+    return {"value": round(2 * m * 8 / mean / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
             "sample": f"n={m} u64 (the full per-GPU workload), 1 warm-up + mean of {trials} "
-                      f"(bench.hpp:41-59), {os.path.basename(O.REF.path)}, avx512={bool(O.REF.ref_avx512_active())}"}
+                      f"(bench.hpp:41-59), {lib}"}
 
 
 # -------------------------------------------------------------------- ours --
-def ours_arm(args, rank, world, local):
+def output_checksum(torch, t, first_word=0):
+    """(sum, wsum) mod 2^64 of a CUDA tensor viewed as u64 words w[i] (u32 zero-extended, 16-byte records as two
+    words), wsum = sum w[i] * (2 * (first_word + i) + 1) -- the checksum of tests/golden/make_bench_checksums.py.
+    int64 products and sums wrap modulo 2^64 on the GPU, which is the arithmetic wanted."""
+    if t.dtype == torch.int32:
+        w = t.reshape(-1).to(torch.int64) & 0xFFFFFFFF
+    else:
+        w = t.reshape(-1).view(torch.int64)
+    s = torch.zeros((), dtype=torch.int64, device=t.device)
+    ws = torch.zeros((), dtype=torch.int64, device=t.device)
+    chunk = 1 << 26
+    for lo in range(0, w.numel(), chunk):
+        x = w[lo:lo + chunk]
+        k = torch.arange(first_word + lo, first_word + lo + x.numel(), dtype=torch.int64, device=t.device)
+        s += x.sum()
+        ws += (x * (2 * k + 1)).sum()
+    return s, ws
+
+
+def hex64(v) -> str:
+    return f"{int(v) & 0xFFFFFFFFFFFFFFFF:016x}"
+
+
+def ours_arm(args, rank, world, local, cpu=None):
     import torch
     import paper_2106_06161_b200 as bsg
     from paper_2106_06161_b200 import _lib
@@ -259,7 +289,16 @@ def ours_arm(args, rank, world, local):
         dominant = "bsg::k_batched"
     else:
         m_total = m_gpu * world  # weak scaling: one global shuffle of N * n elements
-        vals = make_values(torch, m_total, eb, device=dev)  # replicated input
+        # 16-byte records (C5) at N > 1: the input is SHARDED (rank r holds records [r*n, (r+1)*n)) and payload
+        # reads go to peer HBM through CUDA-IPC mappings (NVLink); smaller payloads are replicated.
+        sharded = eb == 16 and world > 1
+        if sharded:
+            from paper_2106_06161_b200 import distributed as D
+            vals = torch.arange(2 * rank * m_gpu, 2 * (rank + 1) * m_gpu, dtype=torch.int64,
+                                device=dev).view(torch.complex128)
+            ipc = D.ipc_shards(vals)
+        else:
+            vals = make_values(torch, m_total, eb, device=dev)  # replicated input
         step_bytes_rank = 2 * m_gpu * eb
         if world == 1:
             out = torch.empty(m_total, dtype=tdt, device=dev)
@@ -277,9 +316,11 @@ def ours_arm(args, rank, world, local):
             counts = torch.zeros(world, dtype=torch.int64, device=dev)
             ccfg = cfg._c()
 
+            src = (None, ctypes.byref(ipc.table)) if sharded else (vals.data_ptr(), None)
+
             def step():
-                _lib.check(_lib.lib.bsg_shuffle_range(m_total, ctypes.byref(ccfg), b.value, e.value, vals.data_ptr(),
-                                                      None, out.data_ptr(), eb, cnt_dev.data_ptr(),
+                _lib.check(_lib.lib.bsg_shuffle_range(m_total, ctypes.byref(ccfg), b.value, e.value, src[0], src[1],
+                                                      out.data_ptr(), eb, cnt_dev.data_ptr(),
                                                       stream.cuda_stream), "shuffle_range")
                 dist.all_gather_into_tensor(counts, cnt_dev)  # the 8-byte count exchange (NCCL)
         pow2 = (m_total & (m_total - 1)) == 0
@@ -364,18 +405,66 @@ def ours_arm(args, rank, world, local):
         except Exception as e:  # noqa: BLE001 -- evidence only
             graph = {"error": str(e)[:200]}
 
-    # Sanity check of the timed output against the library's own index path (cheap, after timing).
-    if not batch and world == 1:
-        perm = bsg.shuffle_indices(min(m_total, 1 << 20), cfg, device=dev)
-        if m_total <= (1 << 20):
-            assert torch.equal(out.to(torch.int64), perm), "bench output mismatch"
+    # Parity of the timed output itself: its checksum against the reference's (tests/golden/bench_checksums.json,
+    # generated from the unmodified reference by tests/golden/make_bench_checksums.py).  At N > 1 each rank
+    # checksums its piece at its global word offset and the pieces are summed over ranks (mod 2^64).
+    torch.cuda.synchronize(dev)
+    if batch:
+        cs, cws = output_checksum(torch, out)
+        key = f"{args.config}@rank{rank}"
+        piece_words = 0
+    else:
+        if world == 1:
+            off_elems, n_elems = 0, m_total
+        else:
+            allc = [int(x) for x in counts.tolist()]
+            off_elems, n_elems = sum(allc[:rank]), allc[rank]
+        k = 2 if eb == 16 else 1
+        cs, cws = output_checksum(torch, out[:n_elems], first_word=off_elems * k)
+        if world > 1:
+            import torch.distributed as dist
+            both = torch.stack([cs, cws])
+            dist.all_reduce(both)  # int64 sums wrap modulo 2^64
+            cs, cws = both[0], both[1]
+        key = f"{args.config}@{world}"
+    gold = ((load_json(os.path.join(ROOT, "tests", "golden", "bench_checksums.json")) or {}).get("configs", {})
+            .get(key))
+    output_check = {"sum": hex64(cs), "wsum": hex64(cws), "golden": key if gold else None,
+                    "what": "checksum of the timed output vs the unmodified reference's output of the same workload"}
+    if gold:
+        output_check["ok"] = gold["sum"] == output_check["sum"] and gold["wsum"] == output_check["wsum"]
+        assert output_check["ok"], f"timed output differs from the reference: {output_check} vs {gold}"
 
     # ---- e2e: public API with pinned HOST buffers, H2D + shuffle + D2H every step.
     # Headline: the streaming C-ABI (bsg_pipeline_*), where step i+1's H2D overlaps step i's D2H;
     # also reported: the synchronous bsg_shuffle_values(host, host) call, one step at a time.
     e2e = None
     e2e_steps = args.e2e_steps or min(args.steps, 6)
-    if not batch:
+    if batch:
+        # the public API with pinned HOST rows: bsg.shuffle_values_batched(host in, out=host out) stages the rows
+        # through device memory (H2D + kernel + D2H) and returns with the result on the host
+        host_in = vals.cpu().pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        bcfg = bsg.ShuffleConfig(seed=SEED + rank * batch, variant=cfg.variant)
+        bsg.shuffle_values_batched(host_in, bcfg, out=host_out)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            bsg.shuffle_values_batched(host_in, bcfg, out=host_out)
+        el = time.perf_counter() - t0
+        assert torch.equal(host_out, out.cpu()), "e2e output mismatch"
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        nb = batch * m_gpu * eb
+        e2e = {"value": round(step_bytes_rank * world / (el / e2e_steps) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "steps": e2e_steps,
+               "ms_per_step": round(el / e2e_steps * 1e3, 3),
+               "path": "bsg_shuffle_values_batched(pinned host rows in, pinned host rows out), synchronous per call"}
+        del host_in, host_out
+    else:
         if world == 1:
             # two host (in, out) pairs so step i+1 never touches step i's buffers; one pair for 16-byte records
             # (2 x 16 GiB pinned), where consecutive steps write the same output bytes
@@ -409,6 +498,32 @@ def ours_arm(args, rank, world, local):
             sync = {"value": round(step_bytes_rank / (sync_ms * 1e-3) / 1e9, 3), "ms_per_step": round(sync_ms, 3),
                     "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call"}
             del pairs
+        elif sharded:
+            # each rank's host holds its input shard: H2D into the IPC-exported device shard, barrier, the
+            # counter-range shuffle reading peers over NVLink, D2H of this rank's output piece
+            host_in = vals.cpu().pin_memory()
+            host_out = torch.empty(out.numel(), dtype=tdt).pin_memory()
+
+            def e2e_step():
+                vals.copy_(host_in, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                dist.barrier()  # every shard is in place before anyone reads a peer
+                step()
+                host_out.copy_(out, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                dist.barrier()  # nobody overwrites its shard while a peer still reads it
+            h2d, d2h = m_gpu * eb, out.numel() * eb
+            e2e_step()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                e2e_step()
+            barrier()
+            el = time.perf_counter() - t0
+            path = ("per rank: H2D of its input shard, counter-range shuffle with payload reads from peer shards "
+                    "over CUDA IPC / NVLink, 8-byte count all-gather, D2H of its output piece")
+            sync = None
+            del host_in, host_out
         else:
             # Distributed data: each rank's host holds one input shard; the global power-of-two shuffle is
             # routed by destination (bsg_route_by_dest), exchanged with one NCCL all-to-all and placed
@@ -447,11 +562,17 @@ def ours_arm(args, rank, world, local):
         if sync:
             e2e["sync"] = sync
 
-    if rank != 0:
+    def finish():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+            if sharded_ipc is not None:
+                sharded_ipc.close()
             dist.destroy_process_group()
+
+    sharded_ipc = ipc if (not batch and sharded) else None
+    if rank != 0:
+        finish()
         return
 
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
@@ -471,8 +592,10 @@ def ours_arm(args, rank, world, local):
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPES[eb], "data": "synthetic (iota values, device-generated)",
-        "config": {"workload": desc + ("" if world == 1 else f"; global shuffle of {world}x n elements, "
-                                                             "counter-range partition, replicated input"),
+        "config": {"workload": desc + ("" if world == 1 or batch else
+                                       f"; global shuffle of {world}x n elements, counter-range partition, "
+                                       + ("input sharded over the ranks, payload read from peer HBM via CUDA IPC"
+                                          if eb == 16 else "replicated input")),
                    "n_per_gpu": m_gpu, "n_total": m_total if not batch else batch * m_gpu * world,
                    "elem_bytes": eb, "seed": SEED, "rounds": 24,
                    "variant": "VariablePhilox" if variant else "Lcg",
@@ -486,6 +609,7 @@ def ours_arm(args, rank, world, local):
                      "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
+        "output_check": output_check,
         "graph_replay": graph,
         "e2e": e2e,
     }
@@ -513,12 +637,9 @@ def ours_arm(args, rank, world, local):
         if gb:
             line["comparators"]["value_over_gather_bound"] = round(value / gb, 3)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_leg(args, args.config)
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
+    finish()
 
 
 def comparators(bsg, torch, dev, vals, out, m, eb, cfg, stream):
@@ -554,13 +675,42 @@ def comparators(bsg, torch, dev, vals, out, m, eb, cfg, stream):
     return res
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` run without a launcher: re-exec this command under torch.distributed.run with one rank
+    per GPU (the same launch the driver uses), so the line is never silently a one-GPU number."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.cpu_leg:
+        print(json.dumps(cpu_baseline_leg(args, args.config)), flush=True)
+        return
     rank, world, local = dist_env()
     if args.impl == "reference":
-        reference_arm(args, rank, world)
+        reference_arm(args, rank, world if "WORLD_SIZE" in os.environ else args.gpus)
         return
-    ours_arm(args, rank, world, local)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
+    # The CPU baseline leg runs first, in its own process, before this process touches the GPU or pins host
+    # memory (a leg run after 16 GiB of cached pinned buffers measured the CPU 1.7x slow in round 1).
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-leg", "--config", args.config],
+                           capture_output=True, text=True)
+        try:
+            cpu = json.loads(r.stdout.strip().splitlines()[-1])
+        except (ValueError, IndexError):
+            cpu = {"error": (r.stderr or r.stdout)[-300:]}
+    ours_arm(args, rank, world, local, cpu)
 
 
 if __name__ == "__main__":

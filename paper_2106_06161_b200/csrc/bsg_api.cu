@@ -279,7 +279,7 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
   // Partitioned path: whole power-of-two domains, and whole non-power-of-two domains with elements <= 8 B
   // (routed by counter, compacted by counter rank in the last pass).
   if (!g_force_compact && g_path != 1 && elem_code > 0 && src.nshards == 0 && c0 == 0 && c1 == (1ULL << bits) &&
-      (pow2 || elem_code <= 8) && bsg::partition_eligible(elem_code, bits) &&
+      (pow2 || elem_code <= 8) && bsg::partition_eligible(elem_code, bits, !pow2) &&
       auto_partition(m, static_cast<uint64_t>(elem_code))) {
     const size_t need = bsg::partition_workspace_bytes(elem_code, bits, !pow2);
     // while capturing, never allocate (it would invalidate the capture): use the workspace only if it is sized

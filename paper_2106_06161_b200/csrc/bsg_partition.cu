@@ -583,6 +583,136 @@ __global__ void __launch_bounds__(kP3Threads) k_place_compact(const T* __restric
   }
 }
 
+// Non-power-of-two last pass, placement by RANK (default).  Window w covers counters [w * 2^14, (w+1) * 2^14)
+// and holds cnt[w] survivors (about half: their counter offsets in od, their values in tv2).  A bitmask of the
+// occupied counter slots (one atomicOr per survivor), its per-word exclusive popcount prefix and one popc give
+// every survivor its rank among the window's survivors -- its output position minus pre[w], i.e. the counter
+// order chained_compact produces (shuffle.hpp:91-147).  Values are placed by rank in a dense shared buffer and
+// written back as one contiguous run.  Against k_place_compact (placement by counter slot, flag bytes, ballots
+// over all 8192 slots of a 64 KiB window) this moves twice the survivors per CTA through the same shared memory
+// and drops the ballot pass.  A window with more than kRankCap survivors (mean 8192, sd 64 for a random
+// bijection; possible for structured ones such as an LCG) is placed in several rounds of kRankCap ranks.
+constexpr int kRankW2 = 14;                    // counters per window (log2)
+constexpr uint32_t kRankWords = 1u << (kRankW2 - 5);  // bitmask words per window (== kP3Threads)
+constexpr uint32_t kRankCap = 8704;            // survivors placed per round (8192 + 8 sd)
+static_assert(kRankWords == kP3Threads, "one bitmask word per thread in the scan");
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, T (&v)[8]) {  // 8 consecutive elements, 16-byte vector loads
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "u32 / u64 payloads");
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int k = 0; k < static_cast<int>(sizeof(T)) * 8 / 16; ++k) {
+    const uint4 x = __ldcs(q + k);
+    reinterpret_cast<uint4*>(v)[k] = x;
+  }
+}
+
+#ifndef BSG_RANK_REG_ROUNDS
+#define BSG_RANK_REG_ROUNDS 2  // survivor rounds (4096 each) whose values stay in registers between the passes
+#endif
+template <typename T>
+__global__ void __launch_bounds__(kP3Threads, BSG_RANK_REG_ROUNDS >= 2 ? 2 : 3)
+    k_place_rank(const T* __restrict__ tv2, const uint16_t* __restrict__ od, const uint32_t* __restrict__ cnt,
+                 const uint32_t* __restrict__ pre, T* __restrict__ out) {
+  constexpr int kRR = BSG_RANK_REG_ROUNDS;
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* win = reinterpret_cast<T*>(smem);                                // kRankCap survivors by rank
+  uint2* wp = reinterpret_cast<uint2*>(win + kRankCap);               // {occupancy word, exclusive prefix}
+  uint32_t* occ = reinterpret_cast<uint32_t*>(wp + kRankWords);      // occupancy bitmask
+  __shared__ uint32_t wt[kP3Threads / 32];
+  const uint32_t w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t c = cnt[w], c8 = c & ~7u;
+  const T* src = tv2 + (static_cast<uint64_t>(w) << kRankW2);
+  const uint16_t* dd = od + (static_cast<uint64_t>(w) << kRankW2);
+  occ[tid] = 0;
+  // Thread t owns survivors [8t, 8t + 8) of each round of 4096 (16-byte loads of offsets and values).  The first
+  // kRR rounds are loaded once, before the occupancy atomics, and stay in registers until they are placed, so the
+  // DRAM latency of the values overlaps the bitmask build and its scan.
+  uint4 sreg[kRR];
+  T vreg[kRR][8];
+#pragma unroll
+  for (int r = 0; r < kRR; ++r) {
+    const uint32_t i0 = 8 * tid + r * 8 * kP3Threads;
+    if (i0 < c8) {
+      sreg[r] = *reinterpret_cast<const uint4*>(dd + i0);
+      load8(src + i0, vreg[r]);
+    }
+  }
+  __syncthreads();  // occ cleared
+  auto mark4 = [&](const uint4& s4) {
+    const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      atomicOr(&occ[(sw[k] & 0xFFFFu) >> 5], 1u << (sw[k] & 31u));
+      atomicOr(&occ[sw[k] >> 21], 1u << ((sw[k] >> 16) & 31u));
+    }
+  };
+#pragma unroll
+  for (int r = 0; r < kRR; ++r)
+    if (8 * tid + r * 8 * kP3Threads < c8) mark4(sreg[r]);
+  for (uint32_t i0 = 8 * tid + kRR * 8 * kP3Threads; i0 < c8; i0 += 8 * kP3Threads)
+    mark4(*reinterpret_cast<const uint4*>(dd + i0));
+  if (c8 + tid < c) {
+    const uint32_t s = dd[c8 + tid];
+    atomicOr(&occ[s >> 5], 1u << (s & 31u));
+  }
+  __syncthreads();
+  // exclusive prefix of the word popcounts (one word per thread)
+  const uint32_t word = occ[tid], pc = __popc(word);
+  uint32_t x = pc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= static_cast<uint32_t>(o)) x += y;
+  }
+  if (lane == 31) wt[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = lane < kP3Threads / 32 ? wt[lane] : 0u;
+    uint32_t z = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, o);
+      if (lane >= static_cast<uint32_t>(o)) z += y;
+    }
+    if (lane < kP3Threads / 32) wt[lane] = z - t;
+  }
+  __syncthreads();
+  wp[tid] = make_uint2(word, wt[warp] + x - pc);
+  __syncthreads();
+  const uint32_t o0 = pre[w];
+  for (uint32_t base = 0; base < c; base += kRankCap) {
+    auto place = [&](uint32_t s, const T& v) {
+      const uint2 q = wp[s >> 5];
+      const uint32_t r = q.y + __popc(q.x & ((1u << (s & 31u)) - 1u)) - base;
+      if (r < kRankCap) win[r] = v;
+    };
+    auto place8 = [&](const uint4& s4, const T (&v)[8]) {
+      const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        place(sw[k] & 0xFFFFu, v[2 * k]);
+        place(sw[k] >> 16, v[2 * k + 1]);
+      }
+    };
+#pragma unroll
+    for (int r = 0; r < kRR; ++r)
+      if (8 * tid + r * 8 * kP3Threads < c8) place8(sreg[r], vreg[r]);
+    for (uint32_t i0 = 8 * tid + kRR * 8 * kP3Threads; i0 < c8; i0 += 8 * kP3Threads) {
+      T v[8];
+      load8(src + i0, v);
+      place8(*reinterpret_cast<const uint4*>(dd + i0), v);
+    }
+    if (c8 + tid < c) place(dd[c8 + tid], src[c8 + tid]);
+    __syncthreads();
+    const uint32_t n = min(kRankCap, c - base);
+    T* o = out + o0 + base;
+    for (uint32_t i = tid; i < n; i += kP3Threads) __stcs(o + i, win[i]);
+    __syncthreads();
+  }
+}
+
 // Window-count prefix, level 1: CTA k scans counts [1024k, 1024k + 1024) into pre[] (chunk-local exclusive
 // prefix) and writes the chunk total; level 2 (k_window_fix) adds the totals of the chunks before each one.
 __global__ void __launch_bounds__(1024) k_window_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pre,
@@ -628,6 +758,10 @@ __global__ void __launch_bounds__(1024) k_window_fix(uint32_t* __restrict__ pre,
   if (i < n) pre[i] += off;
 }
 
+#ifndef BSG_PLACE_RANK
+#define BSG_PLACE_RANK 1  // non-power-of-two last pass: placement by rank (k_place_rank) or by counter slot
+#endif
+
 template <typename T>
 int window_log2() {
   return sizeof(T) == 4 ? 14 : (sizeof(T) == 8 ? 13 : 12);  // 64 KiB smem window
@@ -637,22 +771,26 @@ int window_log2() {
 #ifndef BSG_PART_S1_BIAS
 #define BSG_PART_S1_BIAS 0
 #endif
-void part_split(int bits, int w2, int& s1, int& s2) {
+// Padded domains (about half the counters survive) put the extra bit in the fine fan-out: P1's coarse buckets
+// are counter ranges holding ~half their capacity, and 256 coarse buckets keep P1 at one bin per thread and on
+// its TMA-fed form for cheap bijections (C3: P1 4.13 -> 3.59 ms, C3-LCG 4.25 -> 3.17 ms with 512 fine bins).
+void part_split(int bits, int w2, int& s1, int& s2, bool pad = false) {
   const int total = bits - w2;
-  s1 = (total + 1) / 2 + BSG_PART_S1_BIAS;
+  s1 = (pad ? total / 2 : (total + 1) / 2) + BSG_PART_S1_BIAS;
   s2 = total - s1;
 }
 
 template <int KIND, int D, typename T>
 cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   const int b = a.p.bits;
-  const int w2 = window_log2<T>();
-  int s1, s2;
-  part_split(b, w2, s1, s2);
-  const uint64_t n = 1ULL << b, w1 = 1ULL << (b - s1);
+  const uint64_t n = 1ULL << b;
   const uint64_t m = a.m ? a.m : n;  // inputs; m < n: non-power-of-two domain (only for elements <= 8 B)
   const bool pad = m < n;
   if (pad && sizeof(T) > 8) return cudaErrorNotSupported;
+  const int w2 = pad ? (BSG_PLACE_RANK ? kRankW2 : window_log2<T>()) : window_log2<T>();
+  int s1, s2;
+  part_split(b, w2, s1, s2, pad);
+  const uint64_t w1 = 1ULL << (b - s1);
   const int nb1 = 1 << s1, nb2 = 1 << s2;
   uint32_t* cur1 = a.cursors;
   uint32_t* cur2 = a.cursors + nb1;
@@ -717,10 +855,16 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
       uint32_t* chunk_sum = a.win_prefix + (static_cast<size_t>(kMaxB1) * kMaxB2);
       k_window_scan<<<(nwin + 1023) / 1024, 1024, 0, s>>>(cur2, a.win_prefix, chunk_sum, nwin);
       if (nwin > 1024) k_window_fix<<<(nwin + 1023) / 1024, 1024, 0, s>>>(a.win_prefix, chunk_sum, nwin);
-      const size_t smc = sm3 + (size_t{1} << w2);  // window + one flag byte per counter
-      cudaFuncSetAttribute(k_place_compact<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smc));
-      k_place_compact<T><<<nwin, kP3Threads, smc, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, w2,
-                                                        static_cast<T*>(a.out));
+      if (BSG_PLACE_RANK) {
+        const size_t smr = kRankCap * sizeof(T) + kRankWords * 12;  // survivors by rank + {word, prefix} + bitmask
+        cudaFuncSetAttribute(k_place_rank<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smr));
+        k_place_rank<T><<<nwin, kP3Threads, smr, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out));
+      } else {
+        const size_t smc = sm3 + (size_t{1} << w2);  // window + one flag byte per counter
+        cudaFuncSetAttribute(k_place_compact<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smc));
+        k_place_compact<T><<<nwin, kP3Threads, smc, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, w2,
+                                                          static_cast<T*>(a.out));
+      }
       note_launch(nwin > 1024 ? 6 : 5);
       return cudaGetLastError();
     }
@@ -904,7 +1048,7 @@ cudaError_t launch_route(int elem_code, const RouteLaunch& a, cudaStream_t s) {
   return cudaErrorNotSupported;
 }
 
-bool partition_eligible(int elem_code, int bits) {
+bool partition_eligible(int elem_code, int bits, bool pad) {
   int w2;
   switch (elem_code) {
     case 4: w2 = 14; break;
@@ -912,8 +1056,12 @@ bool partition_eligible(int elem_code, int bits) {
     case 16: w2 = 12; break;
     default: return false;
   }
-  const int total = bits - w2;
-  const int s1 = (total + 1) / 2 + BSG_PART_S1_BIAS, s2 = total - s1;
+  if (pad) {
+    if (elem_code > 8) return false;
+    if (BSG_PLACE_RANK) w2 = kRankW2;
+  }
+  int s1, s2;
+  part_split(bits, w2, s1, s2, pad);
   // fan-outs within the shared-memory histograms; tiles must not straddle buckets; 32-bit destinations
   return bits <= 32 && s1 >= 1 && s2 >= 1 && (1 << s1) <= kMaxB1 && (1 << s2) <= kMaxB2 &&
          (bits - s1) >= kP2TileLog && bits >= 14;

@@ -41,7 +41,7 @@ cudaError_t launch_scatter_simple(int elem_code, const void* in, const uint32_t*
 cudaError_t launch_route(int elem_code, const RouteLaunch& a, cudaStream_t s);
 cudaError_t launch_exclusive_prefix_u64(const unsigned long long* c, unsigned long long* o, int n, cudaStream_t s);
 
-bool partition_eligible(int elem_code, int bits);
+bool partition_eligible(int elem_code, int bits, bool pad = false);
 size_t partition_workspace_bytes(int elem_code, int bits, bool pad = false);
 // Carves the workspace into the launch's temporaries (same layout as partition_workspace_bytes).
 void partition_layout(int elem_code, int bits, bool pad, void* workspace, PartitionLaunch& P);

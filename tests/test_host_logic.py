@@ -119,3 +119,30 @@ def test_bijection_spec_and_splitmix():  # bijection.hpp:146-169, splitmix.hpp:3
     assert all(g.below(7) < 7 for _ in range(100))
     with pytest.raises(bsg.InvalidArgument):
         g.below(0)
+
+
+def test_bench_checksum_matches_fixture_definition():
+    """bench.py's GPU-side output checksum (run here on CPU tensors) equals the generator's numpy definition,
+    for u64 indices, u32 rows and 16-byte records (tests/golden/make_bench_checksums.py)."""
+    import json
+    import os
+    import sys
+
+    import torch
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tests", "golden"))
+    import bench
+    import make_bench_checksums as G
+    perm = np.random.default_rng(5).permutation(1 << 16).astype(np.uint64)
+    s, ws = bench.output_checksum(torch, torch.from_numpy(perm.view(np.int64)), first_word=0)
+    assert (int(s) & (2**64 - 1), int(ws) & (2**64 - 1)) == G.checksum_words(lambda lo, hi: perm[lo:hi], perm.size)
+    rows = perm.astype(np.uint32).reshape(64, -1)
+    s, ws = bench.output_checksum(torch, torch.from_numpy(rows.view(np.int32)))
+    flat = rows.reshape(-1).astype(np.uint64)
+    assert (int(s) & (2**64 - 1), int(ws) & (2**64 - 1)) == G.checksum_words(lambda lo, hi: flat[lo:hi], flat.size)
+    rec = np.stack([perm * np.uint64(2), perm * np.uint64(2) + np.uint64(1)], axis=1).reshape(-1)
+    s, ws = bench.output_checksum(torch, torch.from_numpy(rec.view(np.int64)).view(torch.complex128))
+    assert (int(s) & (2**64 - 1), int(ws) & (2**64 - 1)) == G.checksum_words(lambda lo, hi: rec[lo:hi], rec.size)
+    cfgs = json.load(open(os.path.join(root, "tests", "golden", "bench_checksums.json")))["configs"]
+    for k in ("c1@1", "c2@1", "c2@8", "c3@1", "c3@8", "c2lcg@1", "c3lcg@1", "c5@1", "c4@rank0", "c4@rank7"):
+        assert k in cfgs and len(cfgs[k]["wsum"]) == 16
