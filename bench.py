@@ -326,7 +326,7 @@ def ours_arm(args, rank, world, local, cpu=None):
         pow2 = (m_total & (m_total - 1)) == 0
         partitioned = world == 1 and m_total * eb >= (256 << 20) and eb <= 8  # whole domain, >= 256 MiB
         if partitioned:
-            dominant = "bsg::k_part1+k_part2t+k_place" if pow2 else "bsg::k_part1+k_part2t+k_place_compact"
+            dominant = "bsg::k_part1+k_part2t+k_place" if pow2 else "bsg::k_part1+k_part2t+k_place_rank"
         elif not pow2:
             dominant = "bsg::k_compact_smem"
         else:

@@ -124,6 +124,27 @@ BSG_HD void philox_round(uint32_t& s0, uint32_t& s1, uint32_t k, int L, uint32_t
   }
 }
 
+#ifdef __CUDACC__
+// Forward round with the high product on the FP64 pipe (see inv_high_word below): s0 < 2^L is exact in the
+// biased double, and floor(s0 * M0' / 2^32) has the reference's hi in its low L bits (M0' = M0 mod 2^(32+L)),
+// so one DFMA replaces IMAD.WIDE + IMAD (D == 0) or IMAD.HI + IMAD (D == 1).  Device only, L <= 16.
+template <int D>
+__device__ __forceinline__ void philox_round_f64(uint32_t& s0, uint32_t& s1, uint32_t k, int L, uint32_t LM,
+                                                 uint32_t RM, double hc, double hk) {
+  const uint32_t hi =
+      static_cast<uint32_t>(__double2loint(__fma_rd(__hiloint2double(0x43300000, static_cast<int>(s0)), hc, hk)));
+  if (D == 0) {
+    const uint32_t lo = s0 * kM0Lo;
+    s0 = (hi ^ k ^ s1) & LM;
+    s1 = lo;  // garbage above bit R is masked once at the end
+  } else {
+    const uint32_t lo = (s0 * (kM0Lo << 1)) | (s1 >> L);
+    s0 = (hi ^ k ^ s1) & LM;
+    s1 = lo & RM;
+  }
+}
+#endif
+
 // Inverse round (bijection.hpp:127-141).  For D == 1 the right half carries
 // garbage above bit L+1 between rounds (masked at the end): the spare bit is
 // bit 0 and only `t1 >> 1` modulo 2^L is consumed.

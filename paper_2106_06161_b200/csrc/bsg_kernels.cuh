@@ -463,9 +463,12 @@ __device__ __forceinline__ uint32_t philox_keys_fwd(uint32_t x, const uint32_t* 
 // U counters in lock step (round-major), so the U independent dependency
 // chains interleave instruction by instruction (ptxas keeps a counter-major
 // sequence of unrolled rounds back to back, which stalls on every round).
+#ifndef BSG_BATCHED_F64
+#define BSG_BATCHED_F64 1  // batched kernel: the round's high product on the FP64 pipe (philox_round_f64)
+#endif
 template <int D, int NR, int U>
 __device__ __forceinline__ void philox_keys_fwd_x(uint32_t (&x)[U], const uint32_t* k, int L, int R, uint32_t LM,
-                                                  uint32_t RM) {
+                                                  uint32_t RM, double hc = 0.0, double hk = 0.0) {
   uint32_t s0[U], s1[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -475,7 +478,10 @@ __device__ __forceinline__ void philox_keys_fwd_x(uint32_t (&x)[U], const uint32
 #pragma unroll
   for (int i = 0; i < NR; ++i) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) philox_round<D>(s0[u], s1[u], k[i], L, LM, RM);
+    for (int u = 0; u < U; ++u) {
+      if (BSG_BATCHED_F64) philox_round_f64<D>(s0[u], s1[u], k[i], L, LM, RM, hc, hk);
+      else philox_round<D>(s0[u], s1[u], k[i], L, LM, RM);
+    }
   }
 #pragma unroll
   for (int u = 0; u < U; ++u) x[u] = (s0[u] << R) | (s1[u] & RM);
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
         if constexpr (kRegKeys) {
 #pragma unroll
           for (int u = 0; u < U; ++u) y[u] = c0 + u * NT;
-          philox_keys_fwd_x<D, 24, U>(y, kr, p.L, p.R, p.LM, p.RM);
+          philox_keys_fwd_x<D, 24, U>(y, kr, p.L, p.R, p.LM, p.RM, p.hc, p.hk);
         } else {
 #pragma unroll
           for (int u = 0; u < U; ++u) y[u] = f(c0 + u * NT);
