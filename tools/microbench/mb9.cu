@@ -53,6 +53,31 @@ __device__ __forceinline__ uint32_t inv_dfma(uint32_t y, const BijParams& p, DP 
   return (s0 << p.R) | s1;
 }
 
+// DFMA form with the Z = Y >> sh shift moved to the FMA-heavy pipe as IMAD.HI (Y * 2^L) on rounds where ZSEL
+// says so: ZSEL 1 = every round, 2 = odd rounds.
+template <int D, int ZSEL>
+__device__ __forceinline__ uint32_t inv_dfma_z(uint32_t y, const BijParams& p, DP dp) {
+  const uint32_t sh = p.sh;
+  const uint32_t t0 = y >> p.R, t1 = y & p.RM;
+  uint32_t A = t0 << sh, B = D ? (t1 >> 1) : t1, Z = t1;
+#pragma unroll
+  for (int i = 23; i >= 0; --i) {
+    const uint32_t X = B * p.inv_top;
+    const uint32_t hw = __double2loint(__fma_rd(__hiloint2double(0x43300000, static_cast<int>(X)), dp.c, dp.k));
+    const uint32_t Y = hw ^ p.ktop[i] ^ A;
+    if (D) {
+      B = __funnelshift_rc(Y, Z, sh + 1);
+      Z = (ZSEL == 1 || (ZSEL == 2 && (i & 1))) ? __umulhi(Y, p.shl) : (Y >> sh);
+    } else {
+      B = (ZSEL == 1 || (ZSEL == 2 && (i & 1))) ? __umulhi(Y, p.shl) : (Y >> sh);
+    }
+    A = X;
+  }
+  const uint32_t s0 = A >> sh;
+  const uint32_t s1 = D ? (((B << 1) | (Z & 1u)) & p.RM) : (B & p.RM);
+  return (s0 << p.R) | s1;
+}
+
 // Alternate rounds between the two forms (balances FMA-heavy and FP64 pipes).
 template <int D>
 __device__ __forceinline__ uint32_t inv_mix(uint32_t y, const BijParams& p, DP dp) {
@@ -92,7 +117,9 @@ __global__ void __launch_bounds__(256) k_cipher(BijParams p, DP dp, uint32_t n, 
     uint32_t x;
     if (MODE == 0) x = static_cast<uint32_t>(philox_inv_top<D, 24>(y, p));
     else if (MODE == 1) x = inv_dfma<D>(y, p, dp);
-    else x = inv_mix<D>(y, p, dp);
+    else if (MODE == 2) x = inv_mix<D>(y, p, dp);
+    else if (MODE == 3) x = inv_dfma_z<D, 1>(y, p, dp);
+    else x = inv_dfma_z<D, 2>(y, p, dp);
     acc += x * (2 * y + 1);
   }
   atomicAdd(out, acc);
@@ -105,7 +132,9 @@ __global__ void k_check(BijParams p, DP dp, uint64_t n, unsigned long long* bad)
     const uint32_t a = static_cast<uint32_t>(philox_inv_top<D, 24>(y, p));
     const uint32_t b = inv_dfma<D>(static_cast<uint32_t>(y), p, dp);
     const uint32_t c = inv_mix<D>(static_cast<uint32_t>(y), p, dp);
-    if (a != b || a != c) atomicAdd(bad, 1ull);
+    const uint32_t e = inv_dfma_z<D, 1>(static_cast<uint32_t>(y), p, dp);
+    const uint32_t f = inv_dfma_z<D, 2>(static_cast<uint32_t>(y), p, dp);
+    if (a != b || a != c || a != e || a != f) atomicAdd(bad, 1ull);
   }
 }
 
@@ -151,18 +180,23 @@ int main() {
     BijParams p;
     make_params(kPhilox, bits, 0x5EED, 24, p);
     const DP dp = dfma_consts(p.L);
-    float t0, t1, t2;
+    float t0, t1, t2, t3, t4;
     if (p.R - p.L) {
       t0 = time_it<0, 1>(p, dp, out);
       t1 = time_it<1, 1>(p, dp, out);
       t2 = time_it<2, 1>(p, dp, out);
+      t3 = time_it<3, 1>(p, dp, out);
+      t4 = time_it<4, 1>(p, dp, out);
     } else {
       t0 = time_it<0, 0>(p, dp, out);
       t1 = time_it<1, 0>(p, dp, out);
       t2 = time_it<2, 0>(p, dp, out);
+      t3 = time_it<3, 0>(p, dp, out);
+      t4 = time_it<4, 0>(p, dp, out);
     }
-    printf("bits %d (L=%d R=%d): 2^%d inverse ciphers: IMAD.HI form %.3f ms, DFMA form %.3f ms, alternating %.3f ms\n",
-           bits, p.L, p.R, bits, t0, t1, t2);
+    printf("bits %d (L=%d R=%d): 2^%d inverse ciphers: IMAD.HI form %.3f ms, DFMA form %.3f ms, alternating %.3f ms, "
+           "DFMA + Z on IMAD.HI %.3f ms, DFMA + Z on IMAD.HI every other round %.3f ms\n",
+           bits, p.L, p.R, bits, t0, t1, t2, t3, t4);
   }
   return 0;
 }
