@@ -494,8 +494,12 @@ __device__ __forceinline__ void philox_keys_fwd_x(uint32_t (&x)[U], const uint32
 // blocks give each thread many independent counters (ILP for the 24-round
 // chains, whose keys sit in registers shared by all of them).
 // row_mode: 1 = 16-byte cp.async chunks, 2 = 4-byte chunks, 0 = plain loads.
+// C4 (8192 x 1024 u32, B200): the 24 round keys are read from shared memory each round (one broadcast LDS per
+// round for the thread's 8 counters) so the registers go to the 8 interleaved chains; at 14 CTAs of 64 threads per
+// SM (72 registers) ptxas keeps the chains interleaved: 60 -> 42 us (tools/run_vars.sh; keys in registers at 42
+// registers forced ptxas to run the chains one after another, 69% `wait` stalls).
 #ifndef BSG_BATCHED_MINB64
-#define BSG_BATCHED_MINB64 24  // 39 registers: 24 CTAs (48 warps) per SM, measured ~4% faster for C4
+#define BSG_BATCHED_MINB64 14
 #endif
 template <int KIND, typename T, int NT>
 __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batched(const T* __restrict__ in, T* __restrict__ out, uint64_t batch,
@@ -556,7 +560,10 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
     const uint32_t* keys = s_keys[buf];
     T* row_out = out + b * m;
     const uint64_t sb = seed + b;
-    constexpr bool kRegKeys = kFast;  // 24 keys held in registers, shared by all of the thread's counters
+#ifndef BSG_BATCHED_REGKEYS
+#define BSG_BATCHED_REGKEYS 0
+#endif
+    constexpr bool kRegKeys = kFast && BSG_BATCHED_REGKEYS;  // 24 keys held in registers, shared by all counters
     uint32_t kr[kRegKeys ? 24 : 1];
     if constexpr (kRegKeys) {
 #pragma unroll
@@ -582,6 +589,10 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
 #pragma unroll
           for (int u = 0; u < U; ++u) y[u] = c0 + u * NT;
           philox_keys_fwd_x<D, 24, U>(y, kr, p.L, p.R, p.LM, p.RM, p.hc, p.hk);
+        } else if constexpr (kFast) {  // keys read from shared memory each round (broadcast), registers for chains
+#pragma unroll
+          for (int u = 0; u < U; ++u) y[u] = c0 + u * NT;
+          philox_keys_fwd_x<D, 24, U>(y, keys, p.L, p.R, p.LM, p.RM, p.hc, p.hk);
         } else {
 #pragma unroll
           for (int u = 0; u < U; ++u) y[u] = f(c0 + u * NT);
