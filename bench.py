@@ -619,10 +619,14 @@ def ours_arm(args, rank, world, local, cpu=None):
         line["roofline"]["frac_of_traffic_floor"] = round(traffic / (peak * 1e9) * 1e3 / kernel_ms, 4)
     if dominant.startswith("bsg::k_part1") and variant == 1:
         # Composite floor of the partitioned path: P1 cannot beat the 24-round inverse
-        # cipher on the FMA-heavy pipe (IMAD + IMAD.HI + IMAD = 8 issue cycles per round per warp, measured in
-        # tools/microbench/mb8.cu) nor its own traffic; P2 and P3 cannot beat their traffic at the HBM peak.
+        # cipher nor its own traffic; P2 and P3 cannot beat their traffic at the HBM peak.  Cipher issue floor per
+        # round per warp (tools/microbench/mb8.cu, mb9.cu): odd widths (C2) run the high product on the FP64 pipe
+        # and are bound by the ALU pipe (LOP3 + 2 SHF = 6 cycles); even widths (C3) keep IMAD + IMAD.HI + IMAD on
+        # the FMA-heavy pipe (8 cycles).
         sms, hz = 148, (clk.summary().get("sm_mhz") or 1965) * 1e6
-        cipher_ms = m_total * 24 * 8 / 32 / (sms * 4 * hz) * 1e3
+        bits = (m_total - 1).bit_length()
+        cyc = 6 if bits % 2 else 8
+        cipher_ms = m_total * 24 * cyc / 32 / (sms * 4 * hz) * 1e3
         p1_bytes, p23_bytes = m_total * (eb + eb + 4), m_total * ((eb + 4) + (eb + 2) + (eb + 2) + eb)
         p1_ms = max(cipher_ms, p1_bytes / (peak * 1e9) * 1e3)
         comp = p1_ms + p23_bytes / (peak * 1e9) * 1e3
