@@ -32,6 +32,9 @@ for m, v in (((1 << 16) + 5, 1), ((1 << 16) + 4099, 0), (1 << 16, 0)):  # padded
     vals = torch.arange(m, dtype=torch.int64, device="cuda")
     check(f"partitioned {m} v{v}", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=7, variant=bsg.BijectionVariant(v))
                                                       ).cpu().numpy().view(np.uint64), O.shuffle_indices(m, 7, v, 24))
+vals = torch.arange((1 << 16) + 77, dtype=torch.int32, device="cuda")  # padded u32: k_place_rank<uint32_t>
+check("partitioned u32 padded", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=8)).cpu().numpy().astype(np.uint64),
+      O.shuffle_indices((1 << 16) + 77, 8))
 bsg.set_path(0)
 rows = torch.arange(1024, dtype=torch.int32, device="cuda").repeat(16, 1)
 out = bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=1000)).cpu().numpy()
