@@ -62,6 +62,9 @@ constexpr bool p1_f64() {
   return (KIND == kKindPh0 || KIND == kKindPh1 || KIND == kKindPh0G || KIND == kKindPh1G) &&
          (D ? BSG_P1_F64 != 0 : BSG_P1_F64_D0 != 0);
 }
+#ifndef BSG_RANK2
+#define BSG_RANK2 1  // counting-sort ranks: count with RED, then a returning atomic on the scanned starts
+#endif
 #ifndef BSG_P2_THREADS
 #define BSG_P2_THREADS 256
 #endif
@@ -189,12 +192,18 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) > 8 ? 2 : (p1_f64<KIND, 
     for (int i = 0; i < kP1Items; ++i)
       if (valid(i)) v[i] = __ldcs(in + base + i * kP1Threads);
   }
+  // two-atomic ranks (BSG_RANK2) except for the 2-CTA/SM FP64-cipher form, where the extra barrier costs more
+  // than the start lookup it saves (C2 P1 4.02 vs 3.69 ms; C3 P1 3.56 vs 3.60 ms)
+  constexpr bool kRank2 = BSG_RANK2 && !p1_f64<KIND, D>();
   uint32_t dst[kP1Items], rk[kP1Items];
 #pragma unroll
   for (int i = 0; i < kP1Items; ++i) {
     if constexpr (KIND == kKindDestArray) dst[i] = __ldcs(dsrc + base + i * kP1Threads);
     else dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
-    if (valid(i)) rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
+    if (valid(i)) {
+      if (kRank2) atomicAdd(&hist[dst[i] >> bshift], 1u);  // count only: RED, nothing to wait for
+      else rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
+    }
   }
   __syncthreads();
   // Cursor atomics (nb <= 2 * blockDim) are issued before the scan and consumed after the scatter (latency hidden).
@@ -205,20 +214,39 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) > 8 ? 2 : (p1_f64<KIND, 
     if (i < nb && hist[i]) g[k] = atomicAdd(cur1 + i, hist[i]);
   }
   scan_bins(hist, start, nb, wt);
+  if (kRank2) {
+    // ranks from a second atomic on the scanned starts: one returning shared atomic per element instead of a
+    // returning atomic plus a bank-conflicted start lookup
 #pragma unroll
-  for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
+    for (int k = 0; k < 2; ++k) {
+      const int i = tid + k * kP1Threads;
+      if (i < nb) delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
+    }
+    __syncthreads();  // start[] read for delta before the rank atomics advance it
 #pragma unroll
-  for (int i = 0; i < kP1Items; ++i) {
-    if (!valid(i)) continue;
-    if constexpr (BSG_P1_LATE_LOAD) sv[rk[i]] = __ldcs(in + base + i * kP1Threads);
-    else sv[rk[i]] = v[i];
-    sd[rk[i]] = dst[i];
-  }
+    for (int i = 0; i < kP1Items; ++i) {
+      if (!valid(i)) continue;
+      const uint32_t r = atomicAdd(&start[dst[i] >> bshift], 1u);
+      if constexpr (BSG_P1_LATE_LOAD) sv[r] = __ldcs(in + base + i * kP1Threads);
+      else sv[r] = v[i];
+      sd[r] = dst[i];
+    }
+  } else {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    // one table lookup per element in the write-back: global position = delta[b] + slot
-    const int i = tid + k * kP1Threads;
-    if (i < nb) delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
+    for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
+#pragma unroll
+    for (int i = 0; i < kP1Items; ++i) {
+      if (!valid(i)) continue;
+      if constexpr (BSG_P1_LATE_LOAD) sv[rk[i]] = __ldcs(in + base + i * kP1Threads);
+      else sv[rk[i]] = v[i];
+      sd[rk[i]] = dst[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      // one table lookup per element in the write-back: global position = delta[b] + slot
+      const int i = tid + k * kP1Threads;
+      if (i < nb) delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
+    }
   }
   __syncthreads();
 #pragma unroll 4
@@ -266,7 +294,8 @@ __global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in,
     for (int i = 0; i < kP1Items; ++i) {
       if constexpr (KIND == kKindDestArray) dst[i] = __ldcs(dsrc + base + i * kP1Threads);
       else dst[i] = inv_bij<KIND, D>(base + i * kP1Threads, p);
-      rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
+      if (BSG_RANK2) atomicAdd(&hist[dst[i] >> bshift], 1u);
+      else rk[i] = atomicAdd(&hist[dst[i] >> bshift], 1u);
     }
     __syncthreads();
     uint32_t g[2] = {0u, 0u};
@@ -276,20 +305,39 @@ __global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in,
       if (i < nb && hist[i]) g[k] = atomicAdd(cur1 + i, hist[i]);
     }
     scan_bins(hist, start, nb, wt);
+    if (BSG_RANK2) {
 #pragma unroll
-    for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
-    mbar_wait(&bar, phase);  // this tile's values have landed
+      for (int k = 0; k < 2; ++k) {
+        const int i = tid + k * kP1Threads;
+        if (i < nb) {
+          delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
+          hist[i] = 0;                                                  // next tile
+        }
+      }
+      __syncthreads();  // start[] read for delta before the rank atomics advance it
+      mbar_wait(&bar, phase);  // this tile's values have landed
 #pragma unroll
-    for (int i = 0; i < kP1Items; ++i) {
-      sv[rk[i]] = gv[tid + i * kP1Threads];
-      sd[rk[i]] = dst[i];
-    }
+      for (int i = 0; i < kP1Items; ++i) {
+        const uint32_t r = atomicAdd(&start[dst[i] >> bshift], 1u);
+        sv[r] = gv[tid + i * kP1Threads];
+        sd[r] = dst[i];
+      }
+    } else {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int i = tid + k * kP1Threads;
-      if (i < nb) {
-        delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
-        hist[i] = 0;                                                  // next tile
+      for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
+      mbar_wait(&bar, phase);  // this tile's values have landed
+#pragma unroll
+      for (int i = 0; i < kP1Items; ++i) {
+        sv[rk[i]] = gv[tid + i * kP1Threads];
+        sd[rk[i]] = dst[i];
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int i = tid + k * kP1Threads;
+        if (i < nb) {
+          delta[i] = static_cast<uint32_t>(i * w1) + g[k] - start[i];  // mod 2^32
+          hist[i] = 0;                                                  // next tile
+        }
       }
     }
     __syncthreads();  // staging consumed; sorted tile and delta complete
@@ -438,7 +486,10 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     }
 #pragma unroll
     for (int i = 0; i < kP2Items; ++i)
-      if (tid + i * kP2Threads < static_cast<int>(nv)) rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
+      if (tid + i * kP2Threads < static_cast<int>(nv)) {
+        if (BSG_RANK2) atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
+        else rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
+      }
     __syncthreads();
     // The window-cursor atomics (global, one per window with elements) are issued before the scan and consumed
     // after the scatter, so their L2 round trip overlaps both (it was 9% of P2's stall samples when consumed
@@ -451,19 +502,36 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
       if (q < nb2 && hist[q]) g[k] = atomicAdd(cur + q, hist[q]);
     }
     scan_bins(hist, start, nb2, wt);
-#pragma unroll
-    for (int i = 0; i < kP2Items; ++i) {
-      if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
-      const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
-      if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
-      else sv[s] = gv[tid + i * kP2Threads];
-      sd[s] = d[i];
-    }
     const uint32_t win0 = static_cast<uint32_t>(coarse << w1log);  // positions fit 32 bits (bits <= 32)
+    if (BSG_RANK2) {
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int q = tid + k * kP2Threads;
-      if (q < nb2) delta[q] = win0 + (static_cast<uint32_t>(q) << w2) + g[k] - start[q];
+      for (int k = 0; k < 2; ++k) {
+        const int q = tid + k * kP2Threads;
+        if (q < nb2) delta[q] = win0 + (static_cast<uint32_t>(q) << w2) + g[k] - start[q];
+      }
+      __syncthreads();  // start[] read for delta before the rank atomics advance it
+#pragma unroll
+      for (int i = 0; i < kP2Items; ++i) {
+        if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
+        const uint32_t s = atomicAdd(&start[(d[i] >> w2) & fmask], 1u);
+        if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
+        else sv[s] = gv[tid + i * kP2Threads];
+        sd[s] = d[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kP2Items; ++i) {
+        if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
+        const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
+        if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
+        else sv[s] = gv[tid + i * kP2Threads];
+        sd[s] = d[i];
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int q = tid + k * kP2Threads;
+        if (q < nb2) delta[q] = win0 + (static_cast<uint32_t>(q) << w2) + g[k] - start[q];
+      }
     }
     __syncthreads();  // staging consumed, sorted tile complete, delta ready
     if (tid < nb2) hist[tid] = 0;
