@@ -487,6 +487,54 @@ __device__ __forceinline__ void philox_keys_fwd_x(uint32_t (&x)[U], const uint32
   for (int u = 0; u < U; ++u) x[u] = (s0[u] << R) | (s1[u] & RM);
 }
 
+// Table form of the forward cipher for L == R <= 5 (m <= 1024: the C4 rows).  The round's product words depend
+// only on the L-bit left half, so two 32-entry shared-memory tables hold them for every s0, and the state lives in
+// ONE register: W = (half_h << 16) | (half_l << 2), the two halves alternating roles.
+//   round A (s0 in the low half):  W ^= TA[s0] ^ KA_i,  TA[s0] = hi(s0) << 16 | (lo(s0) ^ s0) << 2
+//   round B (s0 in the high half): W ^= TB[s0] ^ KB_i,  TB[s0] = (lo(s0) ^ s0) << 16 | hi(s0) << 2
+// with hi/lo the reference's high/low product words masked to L bits (bijection.hpp:103-107) and
+// KA_i = k_i << 16, KB_i = k_i << 2 (k_i masked to L bits).  Each XOR sets the new left half
+// hi ^ k ^ s1 in the old right half's place and turns s0 into lo there: bit-exact by construction.  A round is
+// one LDS (32 consecutive words: conflict-free) plus LOP3 (A: index mask) or SHF (B: W >> 14) plus one LOP3 --
+// no IMAD, no DFMA, three issue slots instead of five.
+template <int U>
+__device__ __forceinline__ void philox_tab_fwd_x(uint32_t (&x)[U], const uint32_t* kk, const uint32_t* TA,
+                                                 const uint32_t* TB, int R, uint32_t LM, uint32_t RM, int rounds) {
+  uint32_t W[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) W[u] = ((x[u] & RM) << 16) | ((x[u] >> R) << 2);
+  const uint32_t mA = LM << 2;
+  // byte offsets into the tables: A indexes by W & (LM << 2) (one LOP3), B by W >> 14 (one SHF; the low half is
+  // below 2^7, so bits 14-15 are zero)
+  const char* ta = reinterpret_cast<const char*>(TA);
+  const char* tb = reinterpret_cast<const char*>(TB);
+  auto two = [&](int i) {  // rounds i (A) and i + 1 (B)
+    const uint32_t ka = kk[i], kb = kk[i + 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) W[u] ^= *reinterpret_cast<const uint32_t*>(ta + (W[u] & mA)) ^ ka;
+#pragma unroll
+    for (int u = 0; u < U; ++u) W[u] ^= *reinterpret_cast<const uint32_t*>(tb + (W[u] >> 14)) ^ kb;
+  };
+  int i = 0;
+  if (rounds == 24) {
+#pragma unroll
+    for (int j = 0; j < 24; j += 2) two(j);
+    i = 24;
+  } else {
+    for (; i + 1 < rounds; i += 2) two(i);
+  }
+  if (i < rounds) {  // odd round count: a last A round leaves s0 in the high half
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      W[u] ^= *reinterpret_cast<const uint32_t*>(ta + (W[u] & mA)) ^ kk[i];
+      x[u] = ((W[u] >> 16) << R) | ((W[u] >> 2) & RM);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = (((W[u] >> 2) & LM) << R) | (W[u] >> 16);
+  }
+}
+
 // Rows are double-buffered in shared memory: while shuffle b is evaluated, the
 // row of the CTA's next shuffle streams in with cp.async and its round keys
 // are derived by the first `rounds` threads, so neither the load latency nor
@@ -510,6 +558,21 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
   __shared__ uint32_t s_wcnt[2][(NT / 32)];
   constexpr bool kFast = (KIND == kKindPh0 || KIND == kKindPh1);
   constexpr int D = (KIND == kKindPh1 || KIND == kKindPh1G) ? 1 : 0;
+#ifndef BSG_BATCHED_TAB
+#define BSG_BATCHED_TAB 1
+#endif
+  // table form (philox_tab_fwd_x) for L == R <= 5; keys are then stored pre-shifted per round (KA / KB)
+  constexpr bool kTabKind = BSG_BATCHED_TAB && (KIND == kKindPh0 || KIND == kKindPh0G);
+  __shared__ uint32_t s_tab[kTabKind ? 64 : 1];
+  const bool tab = kTabKind && p.L <= 5;
+  if (tab) {
+    for (int s0 = threadIdx.x; s0 < 32; s0 += NT) {
+      const uint64_t prod = kM0 * static_cast<uint64_t>(s0);
+      const uint32_t hi = static_cast<uint32_t>(prod >> 32) & p.LM, lo = static_cast<uint32_t>(prod) & p.LM;
+      s_tab[s0] = (hi << 16) | ((lo ^ static_cast<uint32_t>(s0)) << 2);       // TA
+      s_tab[32 + s0] = ((lo ^ static_cast<uint32_t>(s0)) << 16) | (hi << 2);  // TB
+    }
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = 1u << p.bits;
   const uint32_t mask32 = n - 1;
@@ -538,7 +601,10 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
   };
   auto make_keys = [&](uint64_t b, int buf) {
     if (KIND != kKindLcg)
-      for (int i = tid; i < p.rounds; i += NT) s_keys[buf][i] = round_key(seed + b, i);
+      for (int i = tid; i < p.rounds; i += NT) {
+        const uint32_t k = round_key(seed + b, i);
+        s_keys[buf][i] = tab ? (k & p.LM) << ((i & 1) ? 2 : 16) : k;
+      }
   };
 
   int buf = 0;
@@ -573,6 +639,13 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
     const uint32_t la = static_cast<uint32_t>((mix64(sb) | 1ULL)) & mask32;
     const uint32_t lc = static_cast<uint32_t>(mix64(sb + 1)) & mask32;
     auto f = [&](uint32_t c) -> uint32_t {
+      if constexpr (kTabKind) {
+        if (tab) {
+          uint32_t y1[1] = {c};
+          philox_tab_fwd_x<1>(y1, keys, s_tab, s_tab + 32, p.R, p.LM, p.RM, kFast ? 24 : p.rounds);
+          return y1[0];
+        }
+      }
       if constexpr (KIND == kKindLcg) return (la * c + lc) & mask32;
       else if constexpr (kRegKeys) return philox_keys_fwd<D, 24>(c, kr, p.L, p.R, p.LM, p.RM, 24);
       else return philox_keys_fwd<D, 0>(c, keys, p.L, p.R, p.LM, p.RM, p.rounds);
@@ -585,7 +658,11 @@ __global__ void __launch_bounds__(NT, NT == 64 ? BSG_BATCHED_MINB64 : 1) k_batch
       constexpr int U = BSG_BATCHED_ILP;
       for (uint32_t c0 = tid; c0 < n; c0 += NT * U) {
         uint32_t y[U];  // counters past n are evaluated, never stored
-        if constexpr (kRegKeys) {
+        if (tab) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) y[u] = c0 + u * NT;
+          philox_tab_fwd_x<U>(y, keys, s_tab, s_tab + 32, p.R, p.LM, p.RM, kFast ? 24 : p.rounds);
+        } else if constexpr (kRegKeys) {
 #pragma unroll
           for (int u = 0; u < U; ++u) y[u] = c0 + u * NT;
           philox_keys_fwd_x<D, 24, U>(y, kr, p.L, p.R, p.LM, p.RM, p.hc, p.hk);

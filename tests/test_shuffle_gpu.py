@@ -328,7 +328,11 @@ def test_batched_vs_oracle_many(bsg, cuda):
     for m, dt, rounds, variant in ((1024, np.uint32, 24, PHILOX), (1000, np.uint64, 24, PHILOX),
                                    (4096, np.uint16, 24, LCG), (3, np.uint8, 24, PHILOX), (777, np.uint32, 12, PHILOX),
                                    (1 << 14, np.uint64, 24, PHILOX), (5000, np.uint32, 31, PHILOX),
-                                   (2, np.uint32, 24, PHILOX), (1 << 17, np.uint32, 24, PHILOX)):
+                                   (2, np.uint32, 24, PHILOX), (1 << 17, np.uint32, 24, PHILOX),
+                                   # shared-memory table rounds (L == R <= 5): odd and generic round counts
+                                   (1000, np.uint32, 25, PHILOX), (64, np.uint32, 3, PHILOX),
+                                   (256, np.uint64, 7, PHILOX), (16, np.uint8, 24, PHILOX),
+                                   (1023, np.uint16, 100, PHILOX)):
         batch = 37
         vals = rng.integers(0, np.iinfo(dt).max, size=(batch, m), dtype=dt)
         got = bsg.shuffle_values_batched(vals, cfg_of(bsg, seed=123, variant=variant, rounds=rounds))
