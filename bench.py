@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-comparators", action="store_true", help="skip gather-bound / CUB sort-shuffle timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(steps, 5))")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: --steps)")
     ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)  # internal: the CPU baseline leg
     return ap.parse_args()
 
@@ -439,7 +439,9 @@ def ours_arm(args, rank, world, local, cpu=None):
     # Headline: the streaming C-ABI (bsg_pipeline_*), where step i+1's H2D overlaps step i's D2H;
     # also reported: the synchronous bsg_shuffle_values(host, host) call, one step at a time.
     e2e = None
-    e2e_steps = args.e2e_steps or min(args.steps, 6)
+    # as many e2e steps as timed device steps: a stream of K shuffles pays the pipeline's fill (the first H2D
+    # alone) and drain (the last D2H alone) once, as a job of K shuffles does
+    e2e_steps = args.e2e_steps or args.steps
     if batch:
         # the public API with pinned HOST rows: bsg.shuffle_values_batched(host in, out=host out) stages the rows
         # through device memory (H2D + kernel + D2H) and returns with the result on the host
@@ -489,9 +491,10 @@ def ours_arm(args, rank, world, local, cpu=None):
             host_in, host_out = pairs[0]
             bsg.shuffle_values_into(host_in, cfg, host_out)
             t1 = time.perf_counter()
-            for _ in range(max(2, e2e_steps // 2)):
+            nsync = max(2, min(e2e_steps, 6) // 2)
+            for _ in range(nsync):
                 bsg.shuffle_values_into(host_in, cfg, host_out)
-            sync_ms = (time.perf_counter() - t1) / max(2, e2e_steps // 2) * 1e3
+            sync_ms = (time.perf_counter() - t1) / nsync * 1e3
             path = (f"bsg_pipeline_submit/wait (C ABI): per step H2D of n*{eb} B from pinned host memory, the "
                     f"shuffle kernels, D2H of n*{eb} B to pinned host memory; 3 streams, 2 device slots, so step "
                     "i+1's H2D overlaps step i's D2H")
