@@ -221,6 +221,11 @@ int32_t bsg_set_force_compact(int32_t on);
  * fused pass, 2 = partitioned whenever eligible (domains of 2^14..2^32
  * counters).  Outputs are identical; returns the old value. */
 int32_t bsg_set_path(int32_t path);
+/* Testing knob: survivors per counter window that the persistent last pass of
+ * padded partitioned shuffles stages in shared memory (default and maximum
+ * 9216); windows holding more take the round-based pass.  Lower it to exercise
+ * that path; outputs are identical.  Returns the old value. */
+uint32_t bsg_set_rank_stage_cap(uint32_t cap);
 /* Bytes of device memory the library currently holds as cached workspaces on
  * the current device (the partitioned path keeps ~14 B per counter for power-of-two
  * domains and ~22 B per counter for padded ones between calls: 7.5 GB after a

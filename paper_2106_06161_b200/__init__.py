@@ -458,6 +458,13 @@ def set_path(path: int) -> int:
     return int(lib.bsg_set_path(int(path)))
 
 
+def set_rank_stage_cap(cap: int) -> int:
+    """Testing knob (bsg_set_rank_stage_cap): survivors per counter window the persistent last pass of padded
+    partitioned shuffles stages in shared memory (default and maximum 9216); windows holding more take the
+    round-based pass.  Outputs are identical."""
+    return int(lib.bsg_set_rank_stage_cap(int(cap)))
+
+
 def set_force_compact(on: bool) -> bool:
     """Testing knob: route power-of-two sizes through the look-back kernel too."""
     return bool(lib.bsg_set_force_compact(1 if on else 0))

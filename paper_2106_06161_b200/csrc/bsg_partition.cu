@@ -680,16 +680,16 @@ __device__ __forceinline__ void load8(const T* p, T (&v)[8]) {  // 8 consecutive
 #define BSG_RANK_REG_ROUNDS 2  // survivor rounds (4096 each) whose values stay in registers between the passes
 #endif
 template <typename T>
-__global__ void __launch_bounds__(kP3Threads, BSG_RANK_REG_ROUNDS >= 2 ? 2 : 3)
-    k_place_rank(const T* __restrict__ tv2, const uint16_t* __restrict__ od, const uint32_t* __restrict__ cnt,
-                 const uint32_t* __restrict__ pre, T* __restrict__ out) {
+__device__ __forceinline__ void place_rank_window(const T* __restrict__ tv2, const uint16_t* __restrict__ od,
+                                                  const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ pre,
+                                                  T* __restrict__ out, const uint32_t w) {
   constexpr int kRR = BSG_RANK_REG_ROUNDS;
   extern __shared__ __align__(16) unsigned char smem[];
   T* win = reinterpret_cast<T*>(smem);                                // kRankCap survivors by rank
   uint2* wp = reinterpret_cast<uint2*>(win + kRankCap);               // {occupancy word, exclusive prefix}
   uint32_t* occ = reinterpret_cast<uint32_t*>(wp + kRankWords);      // occupancy bitmask
   __shared__ uint32_t wt[kP3Threads / 32];
-  const uint32_t w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t c = cnt[w], c8 = c & ~7u;
   const T* src = tv2 + (static_cast<uint64_t>(w) << kRankW2);
   const uint16_t* dd = od + (static_cast<uint64_t>(w) << kRankW2);
@@ -781,6 +781,174 @@ __global__ void __launch_bounds__(kP3Threads, BSG_RANK_REG_ROUNDS >= 2 ? 2 : 3)
   }
 }
 
+// One window per CTA (list == nullptr), or the *nlist windows of list[] (the windows k_place_rank_t leaves over)
+// walked by a small grid.
+template <typename T>
+__global__ void __launch_bounds__(kP3Threads, BSG_RANK_REG_ROUNDS >= 2 ? 2 : 3)
+    k_place_rank(const T* __restrict__ tv2, const uint16_t* __restrict__ od, const uint32_t* __restrict__ cnt,
+                 const uint32_t* __restrict__ pre, T* __restrict__ out, const uint32_t* __restrict__ list,
+                 const uint32_t* __restrict__ nlist) {
+  if (!list) {
+    place_rank_window<T>(tv2, od, cnt, pre, out, blockIdx.x);
+    return;
+  }
+  const uint32_t nw = *nlist;
+  for (uint32_t item = blockIdx.x; item < nw; item += gridDim.x) place_rank_window<T>(tv2, od, cnt, pre, out, list[item]);
+}
+
+// Bulk shared -> global store (TMA engine; bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Non-power-of-two last pass, persistent and TMA-fed (default).  The same placement by rank as k_place_rank, but
+// one 1024-thread CTA per SM walks windows w, w + G, ...: window w's survivors (values and counter offsets) arrive
+// in a staging buffer by two bulk copies on an mbarrier, are read into registers, and the staging buffer at once
+// receives window w + G, so DRAM reads stay in flight while w is marked, scanned and placed.  The placed run goes
+// out by one bulk shared -> global copy (its unaligned head and tail by plain stores) that drains while the next
+// window is ranked.  Windows with more than kRTCap survivors (possible for structured bijections) are appended to
+// list[] for k_place_rank.
+constexpr int kRTThreads = 1024;
+constexpr uint32_t kRTCap = 9216;  // survivors staged per window: 9 per thread (mean 8192, sd 64 for Philox)
+constexpr int kRTItems = kRTCap / kRTThreads;
+}  // namespace
+uint32_t g_rank_stage_cap = kRTCap;
+uint32_t set_rank_stage_cap(uint32_t cap) {
+  const uint32_t old = g_rank_stage_cap;
+  g_rank_stage_cap = std::min(cap, kRTCap);
+  return old;
+}
+namespace {
+
+template <typename T>
+constexpr size_t place_rank_t_smem() {
+  return kRTCap * sizeof(T) + kRTCap * 2 + (kRTCap + 16 / sizeof(T)) * sizeof(T) + kRankWords * 12;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRTThreads, 1)
+    k_place_rank_t(const T* __restrict__ tv2, const uint16_t* __restrict__ od, const uint32_t* __restrict__ cnt,
+                   const uint32_t* __restrict__ pre, T* __restrict__ out, uint32_t nwin, uint32_t* __restrict__ list,
+                   uint32_t* __restrict__ nlist, uint32_t cap) {
+  constexpr uint32_t E = 16 / sizeof(T);  // elements per 16 bytes
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* xv = reinterpret_cast<T*>(smem);                          // staged values
+  uint16_t* xo = reinterpret_cast<uint16_t*>(xv + kRTCap);     // staged counter offsets
+  T* y = reinterpret_cast<T*>(xo + kRTCap);                    // survivors by rank (+ alignment shift)
+  uint2* wp = reinterpret_cast<uint2*>(y + kRTCap + E);        // {occupancy word, exclusive prefix}
+  uint32_t* occ = reinterpret_cast<uint32_t*>(wp + kRankWords);  // occupancy bitmask
+  __shared__ uint32_t wt[32];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kRankWords) occ[tid] = 0;
+  __syncthreads();
+  auto fits = [cap](uint32_t c) { return c > 0 && c <= cap; };  // cap <= kRTCap (lower only to test the list path)
+  auto issue = [&](uint32_t w, uint32_t c) {
+    const uint32_t vb = (c * static_cast<uint32_t>(sizeof(T)) + 15u) & ~15u, ob = (c * 2u + 15u) & ~15u;
+    mbar_expect_tx(&bar, vb + ob);
+    bulk_g2s(xv, tv2 + (static_cast<uint64_t>(w) << kRankW2), vb, &bar);
+    bulk_g2s(xo, od + (static_cast<uint64_t>(w) << kRankW2), ob, &bar);
+  };
+  uint32_t w = blockIdx.x, phase = 0;
+  uint32_t cw = w < nwin ? cnt[w] : 0u;
+  if (tid == 0 && w < nwin && fits(cw)) issue(w, cw);
+  for (; w < nwin; w += gridDim.x) {
+    const uint32_t wn = w + gridDim.x;
+    const uint32_t cn = wn < nwin ? cnt[wn] : 0u;
+    if (!fits(cw)) {  // uniform: nothing staged for this window
+      if (tid == 0) {
+        if (cw > cap) list[atomicAdd(nlist, 1u)] = w;
+        if (wn < nwin && fits(cn)) issue(wn, cn);
+      }
+      cw = cn;
+      continue;
+    }
+    const uint32_t o0 = pre[w];
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    uint32_t so[kRTItems];
+    T v[kRTItems];
+#pragma unroll
+    for (int q = 0; q < kRTItems; ++q) {
+      const uint32_t i = tid + q * kRTThreads;
+      if (i < cw) {
+        so[q] = xo[i];
+        v[q] = xv[i];
+      }
+    }
+    __syncthreads();  // staging consumed by every thread
+    if (tid == 0 && wn < nwin && fits(cn)) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of staging before the refill
+      issue(wn, cn);
+    }
+#pragma unroll
+    for (int q = 0; q < kRTItems; ++q)
+      if (tid + q * kRTThreads < cw) atomicOr(&occ[so[q] >> 5], 1u << (so[q] & 31u));
+    __syncthreads();
+    // exclusive prefix of the word popcounts (threads 0..511, one word each)
+    uint32_t word = 0, pc = 0, x = 0;
+    if (tid < kRankWords) {
+      word = occ[tid];
+      pc = __popc(word);
+      x = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= static_cast<uint32_t>(o)) x += t;
+      }
+      if (lane == 31) wt[warp] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t t = lane < kRankWords / 32 ? wt[lane] : 0u;
+      uint32_t z = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, z, o);
+        if (lane >= static_cast<uint32_t>(o)) z += u;
+      }
+      if (lane < kRankWords / 32) wt[lane] = z - t;
+    }
+    __syncthreads();
+    if (tid < kRankWords) {
+      wp[tid] = make_uint2(word, wt[warp] + x - pc);
+      occ[tid] = 0;  // next window
+    }
+    if (tid == 0) bulk_wait_read();  // the previous window's bulk store has read y
+    __syncthreads();
+    // y[a + r] holds rank r, a = the output run's misalignment in elements, so y + a + head is 16-byte aligned
+    // exactly where out + o0 + head is.
+    const uint32_t a = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(out + o0) & 15u) / sizeof(T));
+#pragma unroll
+    for (int q = 0; q < kRTItems; ++q) {
+      if (tid + q * kRTThreads < cw) {
+        const uint32_t s = so[q];
+        const uint2 e = wp[s >> 5];
+        y[a + e.y + __popc(e.x & ((1u << (s & 31u)) - 1u))] = v[q];
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of y before the bulk read
+    __syncthreads();
+    const uint32_t head = min(cw, (E - a) % E);
+    const uint32_t body = (cw - head) & ~(E - 1u);
+    if (tid == 0 && body) bulk_s2g(out + o0 + head, y + a + head, body * static_cast<uint32_t>(sizeof(T)));
+    if (tid < head) out[o0 + tid] = y[a + tid];
+    const uint32_t t0 = head + body;
+    if (tid >= 32 && tid - 32 < cw - t0) out[o0 + t0 + tid - 32] = y[a + t0 + tid - 32];
+    cw = cn;
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
 // Window-count prefix, level 1: CTA k scans counts [1024k, 1024k + 1024) into pre[] (chunk-local exclusive
 // prefix) and writes the chunk total; level 2 (k_window_fix) adds the totals of the chunks before each one.
 __global__ void __launch_bounds__(1024) k_window_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ pre,
@@ -826,6 +994,9 @@ __global__ void __launch_bounds__(1024) k_window_fix(uint32_t* __restrict__ pre,
   if (i < n) pre[i] += off;
 }
 
+#ifndef BSG_RANK_T
+#define BSG_RANK_T 1  // persistent TMA-fed k_place_rank_t (+ k_place_rank over its overflow windows)
+#endif
 #ifndef BSG_PLACE_RANK
 #define BSG_PLACE_RANK 1  // non-power-of-two last pass: placement by rank (k_place_rank) or by counter slot
 #endif
@@ -862,7 +1033,7 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   const int nb1 = 1 << s1, nb2 = 1 << s2;
   uint32_t* cur1 = a.cursors;
   uint32_t* cur2 = a.cursors + nb1;
-  cudaError_t e = cudaMemsetAsync(a.cursors, 0, kCursorWords * 4, s);
+  cudaError_t e = cudaMemsetAsync(a.cursors, 0, (kCursorWords + 1) * 4, s);  // + the overflow-window count
   if (e != cudaSuccess) return e;
   const size_t sm1 = kP1Tile * (sizeof(T) + 4);
   const size_t sm2 = kP2Tile * (sizeof(T) + 4);
@@ -926,7 +1097,20 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
       if (BSG_PLACE_RANK) {
         const size_t smr = kRankCap * sizeof(T) + kRankWords * 12;  // survivors by rank + {word, prefix} + bitmask
         cudaFuncSetAttribute(k_place_rank<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smr));
-        k_place_rank<T><<<nwin, kP3Threads, smr, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out));
+        if (BSG_RANK_T) {
+          uint32_t* nlist = a.cursors + kCursorWords;
+          constexpr size_t smt = place_rank_t_smem<T>();
+          cudaFuncSetAttribute(k_place_rank_t<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
+          k_place_rank_t<T><<<std::min<uint32_t>(nwin, static_cast<uint32_t>(sms)), kRTThreads, smt, s>>>(
+              p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out), nwin, a.win_list, nlist,
+              std::min(g_rank_stage_cap, kRTCap));
+          k_place_rank<T><<<std::min<uint32_t>(nwin, 2u * static_cast<uint32_t>(sms)), kP3Threads, smr, s>>>(
+              p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out), a.win_list, nlist);
+          note_launch(1);
+        } else {
+          k_place_rank<T><<<nwin, kP3Threads, smr, s>>>(p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out),
+                                                        nullptr, nullptr);
+        }
       } else {
         const size_t smc = sm3 + (size_t{1} << w2);  // window + one flag byte per counter
         cudaFuncSetAttribute(k_place_compact<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smc));
@@ -1145,18 +1329,22 @@ void partition_layout(int elem_code, int bits, bool pad, void* workspace, Partit
   P.tmp_dlow = reinterpret_cast<uint16_t*>(w);
   w += n * 2;
   P.cursors = reinterpret_cast<uint32_t*>(w);
-  w += (kCursorWords * 4 + 255) / 256 * 256;
+  w += ((kCursorWords + 1) * 4 + 255) / 256 * 256;
   if (pad) {
     P.win_prefix = reinterpret_cast<uint32_t*>(w);  // window prefix, then the scan's chunk totals
     w += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 4096 + 255) / 256 * 256;
+    P.win_list = reinterpret_cast<uint32_t*>(w);  // overflow windows of the persistent last pass
+    w += static_cast<size_t>(kMaxB1) * kMaxB2 * 4;
     P.tmp_values2 = w;
   }
 }
 
 size_t partition_workspace_bytes(int elem_code, int bits, bool pad) {
   const uint64_t n = 1ULL << bits;
-  size_t b = n * static_cast<uint64_t>(elem_code) + n * 4 + n * 2 + (kCursorWords * 4 + 255) / 256 * 256;
-  if (pad) b += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 4096 + 255) / 256 * 256 + n * static_cast<uint64_t>(elem_code);
+  size_t b = n * static_cast<uint64_t>(elem_code) + n * 4 + n * 2 + ((kCursorWords + 1) * 4 + 255) / 256 * 256;
+  if (pad)
+    b += (static_cast<size_t>(kMaxB1) * kMaxB2 * 4 + 4096 + 255) / 256 * 256 + static_cast<size_t>(kMaxB1) * kMaxB2 * 4 +
+         n * static_cast<uint64_t>(elem_code);
   return b;
 }
 

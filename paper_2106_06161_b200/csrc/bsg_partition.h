@@ -21,6 +21,7 @@ struct PartitionLaunch {
   uint64_t m = 0;
   void* tmp_values2 = nullptr;     // n * elem bytes
   uint32_t* win_prefix = nullptr;  // n >> window_log2 words
+  uint32_t* win_list = nullptr;    // windows left to the round-based last pass (count at cursors[kCursorWords])
 };
 
 struct RouteLaunch {
@@ -46,5 +47,8 @@ size_t partition_workspace_bytes(int elem_code, int bits, bool pad = false);
 // Carves the workspace into the launch's temporaries (same layout as partition_workspace_bytes).
 void partition_layout(int elem_code, int bits, bool pad, void* workspace, PartitionLaunch& P);
 cudaError_t launch_partition(int elem_code, const PartitionLaunch& a, cudaStream_t s);
+// Testing knob: survivors the persistent last pass of padded domains stages per window (default and maximum
+// 9216); windows above it take the round-based pass.  Returns the old value.
+uint32_t set_rank_stage_cap(uint32_t cap);
 
 }  // namespace bsg

@@ -658,6 +658,31 @@ def test_partitioned_non_power_of_two(bsg, cuda):
         assert np.array_equal(got, O.shuffle_indices(m, m, variant, 24)), (m, variant, dt)
 
 
+def test_partitioned_non_power_of_two_overflow_windows(bsg, cuda):
+    """The persistent last pass stages at most `cap` survivors per 2^14-counter window; windows above it go to
+    the round-based pass through a device list.  Lowering the cap (8192: about half the windows; 0: all of them;
+    8300: a few) must not change the output, for u32/u64, both bijections, and outputs at odd offsets (the bulk
+    store's unaligned head and tail)."""
+    old_path = bsg.set_path(2)
+    old_cap = bsg.set_rank_stage_cap(9216)
+    try:
+        for cap in (8192, 0, 8300, 9216):
+            bsg.set_rank_stage_cap(cap)
+            for m, variant, dt in [((1 << 20) + 1, PHILOX, cuda.int64), ((1 << 19) + 5, LCG, cuda.int32),
+                                   ((1 << 21) - 7, LCG, cuda.int64), (3 * (1 << 17) + 1, PHILOX, cuda.int32)]:
+                vals = cuda.arange(m, dtype=dt, device="cuda")
+                buf = cuda.full((m + 3,), -1, dtype=dt, device="cuda")
+                out = buf[1:m + 1]  # element-aligned, not 16-byte aligned
+                bsg.shuffle_values_into(vals, cfg_of(bsg, seed=m + cap, variant=variant), out)
+                got = out.cpu().numpy().astype(np.int64).view(np.uint64) if dt == cuda.int32 else \
+                    out.cpu().numpy().view(np.uint64)
+                assert np.array_equal(got, O.shuffle_indices(m, m + cap, variant, 24)), (cap, m, variant, dt)
+                assert int(buf[0]) == -1 and int(buf[m + 1]) == -1 and int(buf[m + 2]) == -1, (cap, m)
+    finally:
+        bsg.set_rank_stage_cap(old_cap)
+        bsg.set_path(old_path)
+
+
 def test_partitioned_non_power_of_two_full_size(bsg, cuda):
     """C3 itself (2^29+1 u64, 2^30 counters): the partitioned and single-pass paths agree bit for bit, for the
     Feistel and the LCG; the head matches the oracle."""
