@@ -418,16 +418,17 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) <= 8 ? 3 : 2)
 // loads leaves the per-tile critical path.
 // cnt1 != nullptr (non-power-of-two domains): coarse bucket b holds cnt1[b] <= w1 elements, so tile k of the
 // bucket is partial or empty; empty tiles are skipped before their loads are issued.
-template <typename T>
+template <typename T, int TILE = kP2Tile>
 __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                        T* __restrict__ ov, uint16_t* __restrict__ od,
                                                        uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
                                                        uint32_t ntiles, const uint32_t* __restrict__ cnt1) {
+  constexpr int kItems = TILE / kP2Threads, kTileLog = __builtin_ctz(TILE);
   extern __shared__ __align__(16) unsigned char smem[];
   T* gv = reinterpret_cast<T*>(smem);                    // staging: values of the next tile
-  uint32_t* gd = reinterpret_cast<uint32_t*>(gv + kP2Tile);  // staging: destinations
-  T* sv = reinterpret_cast<T*>(gd + kP2Tile);            // sorted values
-  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP2Tile);  // sorted destinations
+  uint32_t* gd = reinterpret_cast<uint32_t*>(gv + TILE);  // staging: destinations
+  T* sv = reinterpret_cast<T*>(gd + TILE);            // sorted values
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + TILE);  // sorted destinations
   __shared__ uint32_t hist[kMaxB2], start[kMaxB2], wt[32];
   __shared__ uint32_t delta[kMaxB2];
   __shared__ __align__(8) uint64_t bar;
@@ -441,18 +442,18 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
   if (tid + kP2Threads < nb2) hist[tid + kP2Threads] = 0;
   __syncthreads();
   auto issue = [&](uint32_t t) {
-    const uint64_t e0 = static_cast<uint64_t>(t) * kP2Tile;
-    mbar_expect_tx(&bar, kP2Tile * (sizeof(T) + 4));
-    bulk_g2s(gv, tv + e0, kP2Tile * sizeof(T), &bar);
-    bulk_g2s(gd, td + e0, kP2Tile * 4, &bar);
+    const uint64_t e0 = static_cast<uint64_t>(t) * TILE;
+    mbar_expect_tx(&bar, TILE * (sizeof(T) + 4));
+    bulk_g2s(gv, tv + e0, TILE * sizeof(T), &bar);
+    bulk_g2s(gd, td + e0, TILE * 4, &bar);
   };
-  // w1 (coarse bucket capacity) is a power of two >= kP2Tile: shifts, not 64-bit divisions
+  // w1 (coarse bucket capacity) is a power of two >= TILE: shifts, not 64-bit divisions
   const int w1log = 63 - __clzll(static_cast<long long>(w1));
-  const int tpblog = w1log - kP2TileLog;  // log2(tile slots per coarse bucket)
+  const int tpblog = w1log - kTileLog;  // log2(tile slots per coarse bucket)
   auto fill = [&](uint32_t t) -> uint32_t {  // valid elements of tile t (0: empty)
-    if (!cnt1) return kP2Tile;
-    const uint32_t c = cnt1[t >> tpblog], k0 = (t & ((1u << tpblog) - 1)) * kP2Tile;
-    return c > k0 ? min(c - k0, static_cast<uint32_t>(kP2Tile)) : 0u;
+    if (!cnt1) return TILE;
+    const uint32_t c = cnt1[t >> tpblog], k0 = (t & ((1u << tpblog) - 1)) * TILE;
+    return c > k0 ? min(c - k0, static_cast<uint32_t>(TILE)) : 0u;
   };
   auto next = [&](uint32_t t) {
     while (t < ntiles && fill(t) == 0) t += gridDim.x;
@@ -465,15 +466,15 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     mbar_wait(&bar, phase);
     const uint32_t nv = fill(t), tn = next(t + gridDim.x);
     const uint64_t coarse = t >> tpblog;
-    uint32_t d[kP2Items], rk[kP2Items];
+    uint32_t d[kItems], rk[kItems];
 #ifndef BSG_P2T_EARLY
 #define BSG_P2T_EARLY 1
 #endif
     // EARLY: the tile is copied to registers at once, so the staging buffer refills while this tile is ranked,
     // scanned, scattered and written (the whole tile time hides the next load).
-    T v[BSG_P2T_EARLY ? kP2Items : 1];
+    T v[BSG_P2T_EARLY ? kItems : 1];
 #pragma unroll
-    for (int i = 0; i < kP2Items; ++i) {
+    for (int i = 0; i < kItems; ++i) {
       d[i] = gd[tid + i * kP2Threads];
       if constexpr (BSG_P2T_EARLY) v[i] = gv[tid + i * kP2Threads];
     }
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
       }
     }
 #pragma unroll
-    for (int i = 0; i < kP2Items; ++i)
+    for (int i = 0; i < kItems; ++i)
       if (tid + i * kP2Threads < static_cast<int>(nv)) {
         if (BSG_RANK2) atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
         else rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
       }
       __syncthreads();  // start[] read for delta before the rank atomics advance it
 #pragma unroll
-      for (int i = 0; i < kP2Items; ++i) {
+      for (int i = 0; i < kItems; ++i) {
         if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
         const uint32_t s = atomicAdd(&start[(d[i] >> w2) & fmask], 1u);
         if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kP2Items; ++i) {
+      for (int i = 0; i < kItems; ++i) {
         if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
         const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
         if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
@@ -994,6 +995,9 @@ __global__ void __launch_bounds__(1024) k_window_fix(uint32_t* __restrict__ pre,
   if (i < n) pre[i] += off;
 }
 
+#ifndef BSG_P2T16
+#define BSG_P2T16 1  // 16-byte records: the TMA-fed P2 with 2048-element tiles (else the one-tile-per-CTA k_part2)
+#endif
 #ifndef BSG_RANK_T
 #define BSG_RANK_T 1  // persistent TMA-fed k_place_rank_t (+ k_place_rank over its overflow windows)
 #endif
@@ -1079,16 +1083,20 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
                                                          static_cast<uint32_t>(done1));
   // P2 writes the fine windows into `out` itself (power of two: exact sizes) or into a counter-sized buffer.
   T* p2out = pad ? static_cast<T*>(a.tmp_values2) : static_cast<T*>(a.out);
-  if constexpr (sizeof(T) <= 8) {  // TMA-fed persistent P2 (2.65 -> 2.45 ms for C2); 16-byte records keep k_part2
-    const size_t smt = 2 * kP2Tile * (sizeof(T) + 4);
-    cudaFuncSetAttribute(k_part2t<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
+  // TMA-fed persistent P2 (2.65 -> 2.45 ms for C2); 16-byte records stage 2048-element tiles (two stages of
+  // 2048 x 20 B fit twice per SM).
+  constexpr int kTile2 = sizeof(T) <= 8 ? kP2Tile : 2048;
+  if constexpr (sizeof(T) <= 8 || BSG_P2T16) {
+    const size_t smt = 2 * kTile2 * (sizeof(T) + 4);
+    cudaFuncSetAttribute(k_part2t<T, kTile2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
     int per = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T>, kP2Threads, smt);
-    const uint64_t tiles = n / kP2Tile;  // tile slots; in a padded domain the tail of every bucket is empty
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T, kTile2>, kP2Threads, smt);
+    const uint64_t tiles = n / kTile2;  // tile slots; in a padded domain the tail of every bucket is empty
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
-    k_part2t<T><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(tv, a.tmp_dest, p2out, a.tmp_dlow, cur2, w2, nb2,
-                                                                       w1, static_cast<uint32_t>(tiles),
-                                                                       pad ? cur1 : nullptr);
+    k_part2t<T, kTile2><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
+        tv, a.tmp_dest, p2out, a.tmp_dlow, cur2, w2, nb2, w1, static_cast<uint32_t>(tiles), pad ? cur1 : nullptr);
+  }
+  if constexpr (sizeof(T) <= 8) {
     if (pad) {
       const uint32_t nwin = static_cast<uint32_t>(n >> w2);
       uint32_t* chunk_sum = a.win_prefix + (static_cast<size_t>(kMaxB1) * kMaxB2);
@@ -1120,7 +1128,7 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
       note_launch(nwin > 1024 ? 6 : 5);
       return cudaGetLastError();
     }
-  } else {
+  } else if (!BSG_P2T16) {
     k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
                                                                             a.tmp_dlow, cur2, w2, nb2, w1);
   }
