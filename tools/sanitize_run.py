@@ -35,6 +35,16 @@ for m, v in (((1 << 16) + 5, 1), ((1 << 16) + 4099, 0), (1 << 16, 0)):  # padded
 vals = torch.arange((1 << 16) + 77, dtype=torch.int32, device="cuda")  # padded u32: k_place_rank<uint32_t>
 check("partitioned u32 padded", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=8)).cpu().numpy().astype(np.uint64),
       O.shuffle_indices((1 << 16) + 77, 8))
+for cap in (8192, 0):  # windows above the staging cap: the list-driven k_place_rank beside k_place_rank_t
+    old_cap = bsg.set_rank_stage_cap(cap)
+    m = (1 << 16) + 5
+    vals = torch.arange(m, dtype=torch.int64, device="cuda")
+    check(f"partitioned padded cap {cap}", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=11)).cpu().numpy().view(np.uint64),
+          O.shuffle_indices(m, 11))
+    bsg.set_rank_stage_cap(old_cap)
+rec = torch.arange(2 * (1 << 16), dtype=torch.int64, device="cuda").view(-1, 2)  # 16-byte records: k_part2t<uint4>
+got = bsg.shuffle_values(rec.view(torch.complex128), bsg.ShuffleConfig(seed=12)).view(torch.int64).view(-1, 2)
+check("partitioned 16-byte", got[:, 0].cpu().numpy().astype(np.uint64) // 2, O.shuffle_indices(1 << 16, 12))
 bsg.set_path(0)
 rows = torch.arange(1024, dtype=torch.int32, device="cuda").repeat(16, 1)
 out = bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=1000)).cpu().numpy()
