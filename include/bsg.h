@@ -226,6 +226,11 @@ int32_t bsg_set_path(int32_t path);
  * 9216); windows holding more take the round-based pass.  Lower it to exercise
  * that path; outputs are identical.  Returns the old value. */
 uint32_t bsg_set_rank_stage_cap(uint32_t cap);
+/* Testing knob: the partitioned path's last passes write their placed windows
+ * with bulk shared->global copies (1, default) or plain stores (0).  Outputs
+ * are identical; compute-sanitizer's initcheck does not model bulk-copy
+ * writes.  Returns the old value. */
+int32_t bsg_set_bulk_stores(int32_t on);
 /* Bytes of device memory the library currently holds as cached workspaces on
  * the current device (the partitioned path keeps ~14 B per counter for power-of-two
  * domains and ~22 B per counter for padded ones between calls: 7.5 GB after a

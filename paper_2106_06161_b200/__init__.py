@@ -465,6 +465,12 @@ def set_rank_stage_cap(cap: int) -> int:
     return int(lib.bsg_set_rank_stage_cap(int(cap)))
 
 
+def set_bulk_stores(on: bool) -> bool:
+    """Testing knob (bsg_set_bulk_stores): the partitioned path's last passes write their placed windows with bulk
+    shared->global copies (default) or plain stores.  Outputs are identical."""
+    return bool(lib.bsg_set_bulk_stores(1 if on else 0))
+
+
 def set_force_compact(on: bool) -> bool:
     """Testing knob: route power-of-two sizes through the look-back kernel too."""
     return bool(lib.bsg_set_force_compact(1 if on else 0))

@@ -78,6 +78,7 @@ SIGNATURES = {
     "bsg_set_force_compact": (c_int32, [c_int32]),
     "bsg_set_path": (c_int32, [c_int32]),
     "bsg_set_rank_stage_cap": (c_uint32, [c_uint32]),
+    "bsg_set_bulk_stores": (c_int32, [c_int32]),
     "bsg_workspace_bytes": (c_int32, [POINTER(c_uint64)]),
     "bsg_release_workspace": (c_int32, []),
 }

@@ -1053,6 +1053,8 @@ int32_t bsg_set_path(int32_t path) {
 
 uint32_t bsg_set_rank_stage_cap(uint32_t cap) { return bsg::set_rank_stage_cap(cap); }
 
+int32_t bsg_set_bulk_stores(int32_t on) { return bsg::set_bulk_stores(on); }
+
 int32_t bsg_set_force_compact(int32_t on) {
   const int old = g_force_compact;
   g_force_compact = on ? 1 : 0;

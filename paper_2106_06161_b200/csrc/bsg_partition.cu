@@ -553,9 +553,20 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
   }
 }
 
+// Bulk shared -> global store (TMA engine; bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // P3: place each fine window through shared memory, in place in `out`.
 template <typename T>
-__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2) {
+__global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2,
+                                                      int bulk) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* win = reinterpret_cast<T*>(smem);
   const uint32_t W = 1u << w2;
@@ -576,6 +587,15 @@ __global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint1
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (i0 + u * kP3Threads < W) win[d[u]] = v[u];
+  }
+  if (bulk && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {  // the window leaves by one bulk store (TMA engine)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(o, win, W * static_cast<uint32_t>(sizeof(T)));
+      bulk_wait_read();
+    }
+    return;
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < W; i += kP3Threads) __stcs(o + i, win[i]);
@@ -797,16 +817,6 @@ __global__ void __launch_bounds__(kP3Threads, BSG_RANK_REG_ROUNDS >= 2 ? 2 : 3)
   for (uint32_t item = blockIdx.x; item < nw; item += gridDim.x) place_rank_window<T>(tv2, od, cnt, pre, out, list[item]);
 }
 
-// Bulk shared -> global store (TMA engine; bulk-group completion).
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // Non-power-of-two last pass, persistent and TMA-fed (default).  The same placement by rank as k_place_rank, but
 // one 1024-thread CTA per SM walks windows w, w + G, ...: window w's survivors (values and counter offsets) arrive
 // in a staging buffer by two bulk copies on an mbarrier, are read into registers, and the staging buffer at once
@@ -819,6 +829,12 @@ constexpr uint32_t kRTCap = 9216;  // survivors staged per window: 9 per thread 
 constexpr int kRTItems = kRTCap / kRTThreads;
 }  // namespace
 uint32_t g_rank_stage_cap = kRTCap;
+int g_bulk_stores = 1;
+int set_bulk_stores(int on) {
+  const int old = g_bulk_stores;
+  g_bulk_stores = on ? 1 : 0;
+  return old;
+}
 uint32_t set_rank_stage_cap(uint32_t cap) {
   const uint32_t old = g_rank_stage_cap;
   g_rank_stage_cap = std::min(cap, kRTCap);
@@ -835,7 +851,7 @@ template <typename T>
 __global__ void __launch_bounds__(kRTThreads, 1)
     k_place_rank_t(const T* __restrict__ tv2, const uint16_t* __restrict__ od, const uint32_t* __restrict__ cnt,
                    const uint32_t* __restrict__ pre, T* __restrict__ out, uint32_t nwin, uint32_t* __restrict__ list,
-                   uint32_t* __restrict__ nlist, uint32_t cap) {
+                   uint32_t* __restrict__ nlist, uint32_t cap, int bulk) {
   constexpr uint32_t E = 16 / sizeof(T);  // elements per 16 bytes
   extern __shared__ __align__(16) unsigned char smem[];
   T* xv = reinterpret_cast<T*>(smem);                          // staged values
@@ -939,10 +955,10 @@ __global__ void __launch_bounds__(kRTThreads, 1)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes of y before the bulk read
     __syncthreads();
-    const uint32_t head = min(cw, (E - a) % E);
-    const uint32_t body = (cw - head) & ~(E - 1u);
+    const uint32_t head = bulk ? min(cw, (E - a) % E) : cw;
+    const uint32_t body = bulk ? (cw - head) & ~(E - 1u) : 0u;
     if (tid == 0 && body) bulk_s2g(out + o0 + head, y + a + head, body * static_cast<uint32_t>(sizeof(T)));
-    if (tid < head) out[o0 + tid] = y[a + tid];
+    for (uint32_t i = tid; i < head; i += kRTThreads) out[o0 + i] = y[a + i];  // head (all of it without bulk)
     const uint32_t t0 = head + body;
     if (tid >= 32 && tid - 32 < cw - t0) out[o0 + t0 + tid - 32] = y[a + t0 + tid - 32];
     cw = cn;
@@ -1111,7 +1127,7 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
           cudaFuncSetAttribute(k_place_rank_t<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
           k_place_rank_t<T><<<std::min<uint32_t>(nwin, static_cast<uint32_t>(sms)), kRTThreads, smt, s>>>(
               p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out), nwin, a.win_list, nlist,
-              std::min(g_rank_stage_cap, kRTCap));
+              std::min(g_rank_stage_cap, kRTCap), g_bulk_stores);
           k_place_rank<T><<<std::min<uint32_t>(nwin, 2u * static_cast<uint32_t>(sms)), kP3Threads, smr, s>>>(
               p2out, a.tmp_dlow, cur2, a.win_prefix, static_cast<T*>(a.out), a.win_list, nlist);
           note_launch(1);
@@ -1132,7 +1148,8 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
     k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
                                                                             a.tmp_dlow, cur2, w2, nb2, w1);
   }
-  k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2);
+  k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2,
+                                                                       g_bulk_stores);
   note_launch(3);
   return cudaGetLastError();
 }

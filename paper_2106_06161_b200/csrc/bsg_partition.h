@@ -50,5 +50,8 @@ cudaError_t launch_partition(int elem_code, const PartitionLaunch& a, cudaStream
 // Testing knob: survivors the persistent last pass of padded domains stages per window (default and maximum
 // 9216); windows above it take the round-based pass.  Returns the old value.
 uint32_t set_rank_stage_cap(uint32_t cap);
+// Testing knob: the last passes write their placed windows by bulk shared->global copies (default) or by plain
+// stores (compute-sanitizer initcheck does not model bulk-copy writes).  Returns the old value.
+int set_bulk_stores(int on);
 
 }  // namespace bsg

@@ -683,6 +683,28 @@ def test_partitioned_non_power_of_two_overflow_windows(bsg, cuda):
         bsg.set_path(old_path)
 
 
+def test_partitioned_bulk_and_plain_stores_agree(bsg, cuda):
+    """The last passes write placed windows by bulk shared->global copies (default) or plain stores
+    (bsg_set_bulk_stores(0)): both equal the oracle, power of two or padded, aligned or not."""
+    old_path = bsg.set_path(2)
+    old_bulk = bsg.set_bulk_stores(True)
+    try:
+        for bulk in (True, False):
+            bsg.set_bulk_stores(bulk)
+            for m, variant, dt, off in [((1 << 20), PHILOX, cuda.int64, 0), ((1 << 20), LCG, cuda.int32, 1),
+                                        ((1 << 20) + 3, PHILOX, cuda.int64, 1), ((1 << 18) + 9, LCG, cuda.int32, 0)]:
+                vals = cuda.arange(m, dtype=dt, device="cuda")
+                buf = cuda.full((m + 2,), -1, dtype=dt, device="cuda")
+                out = buf[off:off + m]
+                bsg.shuffle_values_into(vals, cfg_of(bsg, seed=m + off, variant=variant), out)
+                got = out.cpu().numpy().astype(np.int64).view(np.uint64) if dt == cuda.int32 else \
+                    out.cpu().numpy().view(np.uint64)
+                assert np.array_equal(got, O.shuffle_indices(m, m + off, variant, 24)), (bulk, m, variant, dt, off)
+    finally:
+        bsg.set_bulk_stores(old_bulk)
+        bsg.set_path(old_path)
+
+
 def test_partitioned_non_power_of_two_full_size(bsg, cuda):
     """C3 itself (2^29+1 u64, 2^30 counters): the partitioned and single-pass paths agree bit for bit, for the
     Feistel and the LCG; the head matches the oracle."""

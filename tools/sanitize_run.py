@@ -7,6 +7,9 @@ import oracle as O
 import paper_2106_06161_b200 as bsg
 from paper_2106_06161_b200 import distributed as D
 
+NO_BULK = os.environ.get("BSG_SAN_NO_BULK") == "1"  # initcheck: plain stores in the last passes
+if NO_BULK:
+    bsg.set_bulk_stores(False)
 ok = True
 def check(name, got, exp):
     global ok
