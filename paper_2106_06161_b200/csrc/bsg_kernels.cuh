@@ -142,25 +142,6 @@ __global__ void __launch_bounds__(kThreads) k_pow2(Src src, void* out_, uint64_t
   constexpr int kTile = kThreads * ITEMS;
   const uint64_t t0 = c0 + static_cast<uint64_t>(blockIdx.x) * kTile + threadIdx.x;
   const bool full = c0 + (static_cast<uint64_t>(blockIdx.x) + 1) * kTile <= c1;
-#ifndef BSG_POW2_PREFETCH_MB
-#define BSG_POW2_PREFETCH_MB 48
-#endif
-  if constexpr (!std::is_same<T, IdxTag>::value && !SH && BSG_POW2_PREFETCH_MB > 0) {
-    // An input that fits in L2 is streamed into it by bulk prefetches (one coalesced slice per CTA) while the
-    // cipher runs, so the random reads below hit L2 instead of opening a DRAM row each (cold inputs).
-    const uint64_t bytes = (p.mask + 1) * sizeof(T);
-    if (threadIdx.x == 0 && bytes <= (static_cast<uint64_t>(BSG_POW2_PREFETCH_MB) << 20) &&
-        (reinterpret_cast<uintptr_t>(src.base) & 15u) == 0) {
-      const uint64_t chunk = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ULL;
-      const uint64_t b0 = chunk * blockIdx.x;
-      if (b0 < bytes) {
-        const uint64_t rest = (bytes - b0) & ~15ULL;
-        const uint32_t len = static_cast<uint32_t>(chunk < rest ? chunk : rest);
-        const uint64_t addr = reinterpret_cast<uint64_t>(src.base) + b0;
-        if (len) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(addr), "r"(len) : "memory");
-      }
-    }
-  }
   CT img[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) img[j] = bij<KIND, CT>(static_cast<CT>(t0 + j * kThreads), p);
