@@ -142,6 +142,9 @@ def main():
             if not os.path.exists(rp):
                 continue
             RS = raw_metrics_all(rp)
+            extra = os.path.join(args.src, f"prof_{cfg}rt.ncu-rep")  # a separate capture of more kernels of it
+            if not suffix and os.path.exists(extra):
+                RS = RS + raw_metrics_all(extra)
             with open(os.path.join(prof, f"{args.round}_ncu_{cfg}{suffix}.json"), "w") as f:
                 json.dump(RS, f, indent=1)
             rd = sum(to_bytes(R["dram__bytes_read.sum"]) for R in RS if "dram__bytes_read.sum" in R)
