@@ -14,6 +14,7 @@ A wrong permutation changes wsum unless (i - j) * (w[i] - w[j]) * 2 vanishes
 mod 2^64 for every displaced pair, impossible for indices and values < 2^34.
 
     python tests/golden/make_bench_checksums.py        # ~15 min on 8 cores, ~20 GB RAM (c5's permutation)
+    python tests/golden/make_bench_checksums.py --c5-multi   # adds c5@2/4/8 (streamed)
 """
 from __future__ import annotations
 
@@ -78,6 +79,54 @@ def streamed_checksum(m, seed, variant, threads=8, chunk=1 << 24):
     return int(s), int(ws)
 
 
+def streamed_checksum_c5(m, seed, threads=8, chunk=1 << 24):
+    """(sum, wsum) of the C5 output for m power-of-two records {2i, 2i+1} (the multi-rank sizes): record k of the
+    output is {2 y, 2 y + 1} with y = philox_apply(k) from the reference, words 2k and 2k + 1."""
+    from concurrent.futures import ThreadPoolExecutor
+    bits = int(O.REF.ref_domain_bits(m))
+    assert (1 << bits) == m
+
+    def part(c0):
+        c = np.arange(c0, min(m, c0 + chunk), dtype=np.uint64)
+        y = np.empty_like(c)
+        assert O.REF.ref_philox_apply_many(bits, seed, 24, c.ctypes.data, c.size, y.ctypes.data) == 0
+        with np.errstate(over="ignore"):
+            two = np.uint64(2)
+            w0, w1 = y * two, y * two + np.uint64(1)
+            i0 = c * two
+            s = np.sum(w0, dtype=np.uint64) + np.sum(w1, dtype=np.uint64)
+            ws = (np.sum(w0 * (i0 * two + np.uint64(1)), dtype=np.uint64) +
+                  np.sum(w1 * (i0 * two + np.uint64(3)), dtype=np.uint64))
+        return s, ws
+
+    s = np.uint64(0)
+    ws = np.uint64(0)
+    with ThreadPoolExecutor(threads) as ex, np.errstate(over="ignore"):
+        starts = list(range(0, m, chunk))
+        for b in range(0, len(starts), threads):
+            for a, w in ex.map(part, starts[b:b + threads]):
+                s += a
+                ws += w
+    return int(s), int(ws)
+
+
+def add_c5_multi():
+    """--c5-multi: add c5@2/4/8 (2^31..2^33 records, streamed) to the committed JSON, the c5@1 entry pinning the
+    streamed form."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "bench_checksums.json")
+    out = json.load(open(path))
+    C = out["configs"]
+    s, ws = streamed_checksum_c5(1 << 30, SEED)
+    assert (f"{s:016x}", f"{ws:016x}") == (C["c5@1"]["sum"], C["c5@1"]["wsum"]), "streamed c5 form"
+    for n in (2, 4, 8):
+        m = (1 << 30) * n
+        s, ws = streamed_checksum_c5(m, SEED)
+        C[f"c5@{n}"] = {"m": m, "variant": 1, "sum": f"{s:016x}", "wsum": f"{ws:016x}"}
+        print("c5", n, C[f"c5@{n}"], flush=True)
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+
+
 def indices(m, seed, variant):
     p = O.ref_shuffle_indices(m, seed, variant, 24)
     assert O.is_valid_permutation(p) if m <= (1 << 24) else True
@@ -134,4 +183,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--c5-multi" in sys.argv:
+        add_c5_multi()
+    else:
+        main()
