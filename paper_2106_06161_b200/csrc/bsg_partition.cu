@@ -68,7 +68,10 @@ constexpr bool p1_f64() {
 #ifndef BSG_P2_THREADS
 #define BSG_P2_THREADS 256
 #endif
-constexpr int kP1Threads = BSG_P1_THREADS, kP1Items = 4096 / BSG_P1_THREADS, kP1Tile = 4096;
+#ifndef BSG_P1_TILE
+#define BSG_P1_TILE 4096
+#endif
+constexpr int kP1Threads = BSG_P1_THREADS, kP1Items = BSG_P1_TILE / BSG_P1_THREADS, kP1Tile = BSG_P1_TILE;
 #ifndef BSG_P2_TILE
 #define BSG_P2_TILE 4096
 #endif
