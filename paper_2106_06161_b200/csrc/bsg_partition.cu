@@ -163,6 +163,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
+// Slot swizzle of the sorted tile buffers: slot r lives at r ^ ((r >> 5) & 31).  Runs of ranks that start at
+// regular offsets (an LCG fills every bin of a tile almost exactly equally, so bin starts fall on multiples of 16)
+// would otherwise put a warp's scatter stores into two banks (up to 9.6x the conflict-free wavefronts, ncu);
+// 32 consecutive slots still map to 32 distinct banks, so the sequential write-back stays conflict-free.
+__device__ __forceinline__ uint32_t swz(uint32_t r) { return r ^ ((r >> 5) & 31u); }
+
+#ifndef BSG_SWZ1
+#define BSG_SWZ1 1  // swizzled sorted buffers in the TMA-fed P1 (cheap bijections)
+#endif
+#ifndef BSG_SWZ2
+#define BSG_SWZ2 0  // ... and in P2
+#endif
+#define SW1(r) (BSG_SWZ1 ? swz(r) : (r))
+#define SW2(r) (BSG_SWZ2 ? swz(r) : (r))
+
 // P1: stream the input, route by coarse destination bucket.
 // PAD: non-power-of-two domain, only inputs j < mv exist (the last tile may be partial); tile0 offsets the
 // tiles of a launch (the partial tail after k_part1t's full tiles).
@@ -290,8 +305,24 @@ __global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in,
   };
   if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
   uint32_t phase = 0;
+#ifndef BSG_P1T_EARLY
+#define BSG_P1T_EARLY 1
+#endif
+  // EARLY: the tile's values are copied to registers as soon as they land and the staging buffer is refilled at
+  // once, so the next tile's load has a whole tile time to arrive (else it is issued after the scatter).
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
     const uint32_t base = t * kP1Tile + tid;
+    T v[BSG_P1T_EARLY ? kP1Items : 1];
+    if constexpr (BSG_P1T_EARLY) {
+      mbar_wait(&bar, phase);
+#pragma unroll
+      for (int i = 0; i < kP1Items; ++i) v[i] = gv[tid + i * kP1Threads];
+      __syncthreads();  // staging consumed
+      if (tid == 0 && t + gridDim.x < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(t + gridDim.x);
+      }
+    }
     uint32_t dst[kP1Items], rk[kP1Items];
 #pragma unroll
     for (int i = 0; i < kP1Items; ++i) {
@@ -318,21 +349,23 @@ __global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in,
         }
       }
       __syncthreads();  // start[] read for delta before the rank atomics advance it
-      mbar_wait(&bar, phase);  // this tile's values have landed
+      if (!BSG_P1T_EARLY) mbar_wait(&bar, phase);  // this tile's values have landed
 #pragma unroll
       for (int i = 0; i < kP1Items; ++i) {
-        const uint32_t r = atomicAdd(&start[dst[i] >> bshift], 1u);
-        sv[r] = gv[tid + i * kP1Threads];
+        const uint32_t r = SW1(atomicAdd(&start[dst[i] >> bshift], 1u));
+        if constexpr (BSG_P1T_EARLY) sv[r] = v[i];
+        else sv[r] = gv[tid + i * kP1Threads];
         sd[r] = dst[i];
       }
     } else {
 #pragma unroll
       for (int i = 0; i < kP1Items; ++i) rk[i] += start[dst[i] >> bshift];
-      mbar_wait(&bar, phase);  // this tile's values have landed
+      if (!BSG_P1T_EARLY) mbar_wait(&bar, phase);  // this tile's values have landed
 #pragma unroll
       for (int i = 0; i < kP1Items; ++i) {
-        sv[rk[i]] = gv[tid + i * kP1Threads];
-        sd[rk[i]] = dst[i];
+        if constexpr (BSG_P1T_EARLY) sv[SW1(rk[i])] = v[i];
+        else sv[SW1(rk[i])] = gv[tid + i * kP1Threads];
+        sd[SW1(rk[i])] = dst[i];
       }
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
@@ -344,15 +377,15 @@ __global__ void __launch_bounds__(kP1Threads) k_part1t(const T* __restrict__ in,
       }
     }
     __syncthreads();  // staging consumed; sorted tile and delta complete
-    if (tid == 0 && t + gridDim.x < ntiles) {
+    if (!BSG_P1T_EARLY && tid == 0 && t + gridDim.x < ntiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(t + gridDim.x);
     }
 #pragma unroll 4
     for (int s = tid; s < kP1Tile; s += kP1Threads) {
-      const uint32_t d = sd[s];
+      const uint32_t d = sd[SW1(s)];
       const uint32_t pos = delta[d >> bshift] + s;
-      __stcs(tv + pos, sv[s]);
+      __stcs(tv + pos, sv[SW1(s)]);
       __stcs(td + pos, d);
     }
     __syncthreads();  // sorted buffers, delta and start reused by the next tile
@@ -517,7 +550,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
         if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
-        const uint32_t s = atomicAdd(&start[(d[i] >> w2) & fmask], 1u);
+        const uint32_t s = SW2(atomicAdd(&start[(d[i] >> w2) & fmask], 1u));
         if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
         else sv[s] = gv[tid + i * kP2Threads];
         sd[s] = d[i];
@@ -526,7 +559,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
         if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
-        const uint32_t s = start[(d[i] >> w2) & fmask] + rk[i];
+        const uint32_t s = SW2(start[(d[i] >> w2) & fmask] + rk[i]);
         if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
         else sv[s] = gv[tid + i * kP2Threads];
         sd[s] = d[i];
@@ -546,9 +579,9 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     }
 #pragma unroll 4
     for (int s = tid; s < static_cast<int>(nv); s += kP2Threads) {
-      const uint32_t dd = sd[s];
+      const uint32_t dd = sd[SW2(s)];
       const uint32_t pos = delta[(dd >> w2) & fmask] + s;
-      ov[pos] = sv[s];
+      ov[pos] = sv[SW2(s)];
       od[pos] = static_cast<uint16_t>(dd & wmask);
     }
     __syncthreads();  // sorted buffers and delta reused by the next tile
