@@ -10,7 +10,11 @@ S = h.index("Warp Stall Sampling (All Samples)")
 W = h.index("L1 Wavefronts Shared")
 WI = h.index("L1 Wavefronts Shared Ideal")
 lines = [r for r in rows[hi + 1:] if r and r[0] not in ("",) and r[0].isdigit()]
-num = lambda x: float(x) if x not in ("", "-") else 0.0  # noqa: E731
+def num(x):
+    try:
+        return float(x)
+    except ValueError:  # "-", "" or a source line of another file section that spilled into the column
+        return 0.0
 tot = sum(num(r[S]) for r in lines)
 print(f"samples {tot:.0f}, shared wavefronts {sum(num(r[W]) for r in lines):.3g} (ideal {sum(num(r[WI]) for r in lines):.3g})")
 for r in sorted(lines, key=lambda r: -num(r[S]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
