@@ -158,6 +158,26 @@ bsg_status bsg_dist_shuffle_values(uint64_t m, const bsg_config* cfg, int32_t ra
 /* Counter range [begin, end) owned by `rank` of `world` for an m-element shuffle. */
 bsg_status bsg_dist_counter_range(uint64_t m, int32_t rank, int32_t world, uint64_t* begin, uint64_t* end);
 
+/* Exchange-partitioned shuffle over two ranks (one process per GPU; DESIGN.md
+ * section 7): the power-of-two domain m = 2^G (2^16..2^32, 4- or 8-byte
+ * elements) is sharded in halves, rank r holding input elements and output
+ * positions [r*m/2, (r+1)*m/2).  Replaces shuffle_values_into
+ * (shuffle.hpp:308-315) for that layout: the concatenated output halves equal
+ * the single-GPU shuffle of the m elements.  Each rank allocates
+ * bsg_xpart_workspace_bytes of device memory, maps its peer's workspace
+ * (bsg_ipc_export/open) and passes both as workspaces[0..1] (rank order).
+ * bsg_xpart_route streams the rank's input half through the inverse cipher
+ * and appends every element to its destination bucket's region in the owner
+ * rank's workspace (peer stores over NVLink, no remote atomics).  After BOTH
+ * ranks' route completed (host barrier), bsg_xpart_place partitions and
+ * places the rank's own buckets into out_half.  Device pointers; both calls
+ * asynchronous on `stream`. */
+bsg_status bsg_xpart_workspace_bytes(uint64_t m, uint32_t elem_bytes, int32_t world, uint64_t* bytes);
+bsg_status bsg_xpart_route(const void* in_half, uint64_t m, uint32_t elem_bytes, const bsg_config* cfg,
+                           int32_t rank, int32_t world, void* const* workspaces, void* stream);
+bsg_status bsg_xpart_place(uint64_t m, uint32_t elem_bytes, int32_t rank, int32_t world,
+                           void* const* workspaces, void* out_half, void* stream);
+
 /* Sharded power-of-two shuffle by destination routing: the
  * local elements global_offset .. global_offset+n_local-1 of an m-element
  * shuffle (m = 2^bits <= 2^32) are grouped by the part owning their output

@@ -78,6 +78,10 @@ SIGNATURES = {
     "bsg_set_force_compact": (c_int32, [c_int32]),
     "bsg_set_path": (c_int32, [c_int32]),
     "bsg_set_rank_stage_cap": (c_uint32, [c_uint32]),
+    "bsg_xpart_workspace_bytes": (c_int32, [c_uint64, c_uint32, c_int32, POINTER(c_uint64)]),
+    "bsg_xpart_route": (c_int32, [c_void_p, c_uint64, c_uint32, POINTER(bsg_config), c_int32, c_int32,
+                                  POINTER(c_void_p), c_void_p]),
+    "bsg_xpart_place": (c_int32, [c_uint64, c_uint32, c_int32, c_int32, POINTER(c_void_p), c_void_p, c_void_p]),
     "bsg_set_bulk_stores": (c_int32, [c_int32]),
     "bsg_workspace_bytes": (c_int32, [POINTER(c_uint64)]),
     "bsg_release_workspace": (c_int32, []),

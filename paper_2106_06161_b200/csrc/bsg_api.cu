@@ -805,6 +805,71 @@ bsg_status bsg_route_by_dest(const void* in, uint64_t n_local, uint64_t global_o
   });
 }
 
+namespace {
+bsg_status xpart_check(uint64_t m, uint32_t elem_bytes, int32_t world, int* G) {
+  if (m < 16 || (m & (m - 1))) return fail(BSG_EINVAL, "xpart: m must be a power of two >= 16");
+  *G = bsg::domain_bits(m);
+  if (!bsg::xpart_eligible(static_cast<int>(elem_bytes), *G, world))
+    return fail(BSG_EUNSUPPORTED, "xpart: two ranks, 4- or 8-byte elements, 2^16 <= m <= 2^32");
+  return BSG_OK;
+}
+}  // namespace
+
+bsg_status bsg_xpart_workspace_bytes(uint64_t m, uint32_t elem_bytes, int32_t world, uint64_t* bytes) {
+  int G = 0;
+  BSG_TRY(xpart_check(m, elem_bytes, world, &G));
+  if (!bytes) return fail(BSG_EINVAL, "null pointer");
+  *bytes = bsg::xpart_workspace_bytes(static_cast<int>(elem_bytes), G);
+  return BSG_OK;
+}
+
+bsg_status bsg_xpart_route(const void* in_half, uint64_t m, uint32_t elem_bytes, const bsg_config* cfg_in,
+                           int32_t rank, int32_t world, void* const* workspaces, void* stream) {
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  int G = 0;
+  BSG_TRY(xpart_check(m, elem_bytes, world, &G));
+  if (rank < 0 || rank >= world) return fail(BSG_EINVAL, "xpart: rank outside [0, world)");
+  if (!in_half || !workspaces || !workspaces[0] || !workspaces[1]) return fail(BSG_EINVAL, "null pointer");
+  BijParams p;
+  BSG_TRY(build_params(cfg.variant, G, cfg.seed, cfg.num_rounds, p));
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (!is_device_ptr(in_half)) return fail(BSG_EINVAL, "xpart_route: device pointers only");
+    bsg::XpartLaunch X;
+    X.in = in_half;
+    X.ws[0] = workspaces[0];
+    X.ws[1] = workspaces[1];
+    X.G = G;
+    X.rank = rank;
+    X.p = p;
+    BSG_TRY(ws_begin(c, s));
+    BSG_TRY(upload_keys(c, X.p, cfg.seed, s));
+    BSG_CUDA(bsg::launch_xpart_route(static_cast<int>(elem_bytes), X, s));
+    BSG_TRY(ws_end(c, s));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_xpart_place(uint64_t m, uint32_t elem_bytes, int32_t rank, int32_t world, void* const* workspaces,
+                           void* out_half, void* stream) {
+  int G = 0;
+  BSG_TRY(xpart_check(m, elem_bytes, world, &G));
+  if (rank < 0 || rank >= world) return fail(BSG_EINVAL, "xpart: rank outside [0, world)");
+  if (!out_half || !workspaces || !workspaces[0] || !workspaces[1]) return fail(BSG_EINVAL, "null pointer");
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    cudaStream_t s = as_stream(stream);
+    if (!is_device_ptr(out_half)) return fail(BSG_EINVAL, "xpart_place: device pointers only");
+    bsg::XpartLaunch X;
+    X.out = out_half;
+    X.ws[0] = workspaces[0];
+    X.ws[1] = workspaces[1];
+    X.G = G;
+    X.rank = rank;
+    BSG_CUDA(bsg::launch_xpart_place(static_cast<int>(elem_bytes), X, s));
+    return BSG_OK;
+  });
+}
+
 bsg_status bsg_scatter_permutation(const void* values, const uint32_t* dest, uint64_t n, void* out,
                                    uint32_t elem_bytes, void* stream) {
   if (n == 0) return BSG_OK;

@@ -458,7 +458,8 @@ template <typename T, int TILE = kP2Tile>
 __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                        T* __restrict__ ov, uint16_t* __restrict__ od,
                                                        uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
-                                                       uint32_t ntiles, const uint32_t* __restrict__ cnt1) {
+                                                       uint32_t ntiles, const uint32_t* __restrict__ cnt1,
+                                                       int rsh = 0) {
   constexpr int kItems = TILE / kP2Threads, kTileLog = __builtin_ctz(TILE);
   extern __shared__ __align__(16) unsigned char smem[];
   T* gv = reinterpret_cast<T*>(smem);                    // staging: values of the next tile
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
   for (; t < ntiles; phase ^= 1) {
     mbar_wait(&bar, phase);
     const uint32_t nv = fill(t), tn = next(t + gridDim.x);
-    const uint64_t coarse = t >> tpblog;
+    const uint64_t coarse = (t >> tpblog) >> rsh;  // rsh: 2^rsh regions per coarse bucket (exchange path)
     uint32_t d[kItems], rk[kItems];
 #ifndef BSG_P2T_EARLY
 #define BSG_P2T_EARLY 1
@@ -1203,6 +1204,204 @@ cudaError_t dispatch_partition(const PartitionLaunch& a, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+}  // namespace
+
+// ------------------------------------------------------------------------
+// Exchange partition (two ranks, power-of-two domain of 2^G counters, input sharded in two halves): the
+// partitioned path with its first pass writing across the pair.  Rank r streams its input half (global indices
+// j = r * 2^(G-1) + i), computes f^-1(j) once per element and counting-sorts each tile into the 2 * 2^s1 coarse
+// buckets of the GLOBAL domain; buckets [0, 2^s1) are rank 0's output half, the rest rank 1's.  A bucket's
+// owner holds one region per source rank (capacity = the bucket span, so no count pass is needed), and the
+// source appends to its own region with its own cursors: peer traffic is plain stores (NVLink) with no remote
+// atomics.  After both ranks' P1, each owner reads the two sources' cursors as region fills and runs P2 (regions
+// of one bucket share its window cursors) and P3 on its own 2^(G-1) outputs.  The output half of rank r is
+// out[r * 2^(G-1), (r + 1) * 2^(G-1)) of the single-GPU shuffle of all 2^G elements.
+namespace {
+template <int KIND, int D, typename T>
+__global__ void __launch_bounds__(kP1Threads, p1_f64<KIND, D>() ? BSG_P1_MINB_F64 : BSG_P1_MINB)
+    k_part1x(const T* __restrict__ in, uint32_t j0, T* __restrict__ tv0, T* __restrict__ tv1,
+             uint32_t* __restrict__ td0, uint32_t* __restrict__ td1, uint32_t* __restrict__ cur, BijParams p,
+             int bshift, int s1, int src) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* sv = reinterpret_cast<T*>(smem);
+  uint32_t* sd = reinterpret_cast<uint32_t*>(sv + kP1Tile);
+  __shared__ uint32_t hist[kMaxB1], start[kMaxB1], wt[32];
+  __shared__ uint32_t delta[kMaxB1];
+  const int tid = threadIdx.x, nb = 2 << s1;
+  for (int i = tid; i < nb; i += kP1Threads) hist[i] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kP1Tile + tid;  // local index
+  uint32_t dst[kP1Items];
+#pragma unroll
+  for (int i = 0; i < kP1Items; ++i) {
+    dst[i] = inv_bij<KIND, D>(j0 + base + i * kP1Threads, p);
+    atomicAdd(&hist[dst[i] >> bshift], 1u);
+  }
+  __syncthreads();
+  uint32_t g[2] = {0u, 0u};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = tid + k * kP1Threads;
+    if (i < nb && hist[i]) g[k] = atomicAdd(cur + i, hist[i]);  // this source's cursor of global bucket i
+  }
+  scan_bins(hist, start, nb, wt);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = tid + k * kP1Threads;
+    // region (bucket i within its owner, source) of capacity 2^bshift in the owner's arrays
+    if (i < nb) delta[i] = ((((static_cast<uint32_t>(i) & ((1u << s1) - 1u)) << 1) | static_cast<uint32_t>(src))
+                            << bshift) + g[k] - start[i];  // mod 2^32
+  }
+  __syncthreads();  // start[] read for delta before the rank atomics advance it
+#pragma unroll
+  for (int i = 0; i < kP1Items; ++i) {
+    const uint32_t r = atomicAdd(&start[dst[i] >> bshift], 1u);
+    sv[r] = __ldcs(in + base + i * kP1Threads);
+    sd[r] = dst[i];
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int s = tid; s < kP1Tile; s += kP1Threads) {
+    const uint32_t d = sd[s];
+    const uint32_t b = d >> bshift;
+    const uint32_t pos = delta[b] + s;
+    const bool peer1 = (b >> s1) != 0;  // owner rank of the bucket
+    __stcs((peer1 ? tv1 : tv0) + pos, sv[s]);
+    __stcs((peer1 ? td1 : td0) + pos, d);
+  }
+}
+
+// Region fills of the owner's buckets: region (b, src) holds the count source src appended to global bucket
+// owner * 2^s1 + b (that source's cursor, read from its workspace -- a peer mapping for the other rank).
+__global__ void k_xfill(const uint32_t* __restrict__ cur_src0, const uint32_t* __restrict__ cur_src1,
+                        uint32_t* __restrict__ cnt1, int s1, int owner) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (2 << s1)) return;
+  const int b = (owner << s1) + (q >> 1);
+  cnt1[q] = (q & 1) ? cur_src1[b] : cur_src0[b];
+}
+
+struct XLayout {
+  int G, Lb, w2, s1, s2;
+  size_t tv, td, dlow, cur, cur2, cnt1, total;
+};
+XLayout xlayout(int elem_code, int G) {
+  XLayout L{};
+  L.G = G;
+  L.Lb = G - 1;
+  L.w2 = elem_code == 4 ? 14 : 13;
+  part_split(L.Lb, L.w2, L.s1, L.s2);
+  const uint64_t R = 2ULL << L.Lb;  // region slots: two sources per bucket
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t o = 0;
+  L.tv = o;
+  o = al(o + R * static_cast<uint64_t>(elem_code));
+  L.td = o;
+  o = al(o + R * 4);
+  L.dlow = o;
+  o = al(o + (1ULL << L.Lb) * 2);
+  L.cur = o;
+  o = al(o + (2u << L.s1) * 4);
+  L.cur2 = o;
+  o = al(o + (static_cast<size_t>(1) << (L.s1 + L.s2)) * 4);
+  L.cnt1 = o;
+  o = al(o + (2u << L.s1) * 4);
+  L.total = o;
+  return L;
+}
+}  // namespace
+
+bool xpart_eligible(int elem_code, int G, int world) {
+  if (world != 2 || (elem_code != 4 && elem_code != 8) || G < 16 || G > 32) return false;
+  const XLayout L = xlayout(elem_code, G);
+  return L.s1 >= 1 && L.s2 >= 1 && (2 << L.s1) <= kMaxB1 && (1 << L.s2) <= kMaxB2 &&
+         (L.Lb - L.s1) >= kP2TileLog && ((1ULL << L.Lb) % kP1Tile) == 0;
+}
+
+size_t xpart_workspace_bytes(int elem_code, int G) { return xlayout(elem_code, G).total; }
+
+namespace {
+template <int KIND, int D, typename T>
+cudaError_t run_xroute(const XpartLaunch& a, cudaStream_t s) {
+  const XLayout L = xlayout(sizeof(T), a.G);
+  char* w[2] = {static_cast<char*>(a.ws[0]), static_cast<char*>(a.ws[1])};
+  uint32_t* cur = reinterpret_cast<uint32_t*>(w[a.rank] + L.cur);
+  cudaError_t e = cudaMemsetAsync(cur, 0, (2u << L.s1) * 4, s);
+  if (e != cudaSuccess) return e;
+  const size_t sm1 = kP1Tile * (sizeof(T) + 4);
+  cudaFuncSetAttribute(k_part1x<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1));
+  const uint64_t n_local = 1ULL << L.Lb;
+  k_part1x<KIND, D, T><<<static_cast<unsigned>(n_local / kP1Tile), kP1Threads, sm1, s>>>(
+      static_cast<const T*>(a.in), static_cast<uint32_t>(static_cast<uint64_t>(a.rank) << L.Lb),
+      reinterpret_cast<T*>(w[0] + L.tv), reinterpret_cast<T*>(w[1] + L.tv), reinterpret_cast<uint32_t*>(w[0] + L.td),
+      reinterpret_cast<uint32_t*>(w[1] + L.td), cur, a.p, L.Lb - L.s1, L.s1, a.rank);
+  note_launch(1);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t run_xplace(const XpartLaunch& a, cudaStream_t s) {
+  const XLayout L = xlayout(sizeof(T), a.G);
+  char* me = static_cast<char*>(a.ws[a.rank]);
+  uint32_t* cnt1 = reinterpret_cast<uint32_t*>(me + L.cnt1);
+  uint32_t* cur2 = reinterpret_cast<uint32_t*>(me + L.cur2);
+  cudaError_t e = cudaMemsetAsync(cur2, 0, (static_cast<size_t>(1) << (L.s1 + L.s2)) * 4, s);
+  if (e != cudaSuccess) return e;
+  k_xfill<<<((2 << L.s1) + 255) / 256, 256, 0, s>>>(
+      reinterpret_cast<const uint32_t*>(static_cast<char*>(a.ws[0]) + L.cur),
+      reinterpret_cast<const uint32_t*>(static_cast<char*>(a.ws[1]) + L.cur), cnt1, L.s1, a.rank);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smt = 2 * kP2Tile * (sizeof(T) + 4);
+  cudaFuncSetAttribute(k_part2t<T, kP2Tile>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
+  int per = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T, kP2Tile>, kP2Threads, smt);
+  const uint64_t w1 = 1ULL << (L.Lb - L.s1);
+  const uint64_t tiles = (2ULL << L.Lb) / kP2Tile;  // region tile slots (two regions per bucket)
+  const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
+  uint16_t* dlow = reinterpret_cast<uint16_t*>(me + L.dlow);
+  k_part2t<T, kP2Tile><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
+      reinterpret_cast<const T*>(me + L.tv), reinterpret_cast<const uint32_t*>(me + L.td), static_cast<T*>(a.out),
+      dlow, cur2, L.w2, 1 << L.s2, w1, static_cast<uint32_t>(tiles), cnt1, 1);
+  const size_t sm3 = (size_t{1} << L.w2) * sizeof(T);
+  cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+  k_place<T><<<static_cast<unsigned>((1ULL << L.Lb) >> L.w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), dlow,
+                                                                                    L.w2, g_bulk_stores);
+  note_launch(3);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch_xroute(const XpartLaunch& a, cudaStream_t s) {
+  switch (kind_of(a.p)) {
+    case kKindLcg: return run_xroute<kKindLcg, 0, T>(a, s);
+    case kKindPh0: return run_xroute<kKindPh0, 0, T>(a, s);
+    case kKindPh1: return run_xroute<kKindPh1, 1, T>(a, s);
+    case kKindPh0G: return run_xroute<kKindPh0G, 0, T>(a, s);
+    case kKindPh1G: return run_xroute<kKindPh1G, 1, T>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_xpart_route(int elem_code, const XpartLaunch& a, cudaStream_t s) {
+  switch (elem_code) {
+    case 4: return dispatch_xroute<uint32_t>(a, s);
+    case 8: return dispatch_xroute<uint64_t>(a, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_xpart_place(int elem_code, const XpartLaunch& a, cudaStream_t s) {
+  switch (elem_code) {
+    case 4: return run_xplace<uint32_t>(a, s);
+    case 8: return run_xplace<uint64_t>(a, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+namespace {
 
 // ------------------------------------------------------------------------
 // Route-by-destination (multi-GPU sharded power-of-two shuffle):

@@ -42,6 +42,20 @@ cudaError_t launch_scatter_simple(int elem_code, const void* in, const uint32_t*
 cudaError_t launch_route(int elem_code, const RouteLaunch& a, cudaStream_t s);
 cudaError_t launch_exclusive_prefix_u64(const unsigned long long* c, unsigned long long* o, int n, cudaStream_t s);
 
+// Exchange partition over two ranks (bsg_xpart_*): rank r's input half, both ranks' workspaces (one local,
+// one peer mapping), rank r's output half; G = log2 of the global power-of-two domain.
+struct XpartLaunch {
+  const void* in = nullptr;
+  void* out = nullptr;
+  void* ws[2] = {nullptr, nullptr};
+  int G = 0, rank = 0;
+  BijParams p;
+};
+bool xpart_eligible(int elem_code, int G, int world);
+size_t xpart_workspace_bytes(int elem_code, int G);
+cudaError_t launch_xpart_route(int elem_code, const XpartLaunch& a, cudaStream_t s);
+cudaError_t launch_xpart_place(int elem_code, const XpartLaunch& a, cudaStream_t s);
+
 bool partition_eligible(int elem_code, int bits, bool pad = false);
 size_t partition_workspace_bytes(int elem_code, int bits, bool pad = false);
 // Carves the workspace into the launch's temporaries (same layout as partition_workspace_bytes).

@@ -227,3 +227,82 @@ def ipc_shards(local_shard, group=None) -> IpcShards:
     tab.count = world
     tab.shard_elems = sizes.pop()
     return IpcShards(tab, opened)
+
+
+class ExchangeShuffle:
+    """Two-rank exchange-partitioned shuffle of a power-of-two domain sharded in halves (bsg_xpart_*, DESIGN.md
+    section 7): rank r holds input elements and output positions [r*m/2, (r+1)*m/2).  Each rank streams its input
+    half through the inverse cipher once and appends every element to its destination bucket's region in the
+    owner rank's workspace (peer stores through a CUDA-IPC mapping, NVLink between GPUs, no remote atomics); then
+    each rank partitions and places its own buckets.  The concatenated halves equal the single-GPU shuffle.
+    The workspaces are allocated and mapped once (m and the element type fixed); `close()` unmaps the peer's."""
+
+    def __init__(self, m: int, dtype, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.m = int(m)
+        self.itemsize = torch.empty((), dtype=dtype).element_size()
+        nbytes = ctypes.c_uint64()
+        check(lib.bsg_xpart_workspace_bytes(self.m, self.itemsize, self.world, ctypes.byref(nbytes)),
+              "xpart_workspace_bytes")
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws = torch.empty(nbytes.value, dtype=torch.uint8, device=device)
+        h = (ctypes.c_ubyte * IPC_HANDLE_BYTES)()
+        check(lib.bsg_ipc_export(self.ws.data_ptr(), h), "ipc_export")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self._opened = []
+        self.ptrs = (ctypes.c_void_p * self.world)()
+        for g, hb in enumerate(handles):
+            if g == self.rank:
+                self.ptrs[g] = self.ws.data_ptr()
+                continue
+            p = ctypes.c_void_p()
+            check(lib.bsg_ipc_open((ctypes.c_ubyte * IPC_HANDLE_BYTES).from_buffer_copy(hb), ctypes.byref(p)),
+                  "ipc_open")
+            self._opened.append(p.value)
+            self.ptrs[g] = p.value
+
+    def route(self, local_half, cfg: ShuffleConfig):
+        """Pass 1 of this rank (asynchronous on the current stream)."""
+        import torch
+        stream = torch.cuda.current_stream(local_half.device).cuda_stream
+        check(lib.bsg_xpart_route(local_half.data_ptr(), self.m, self.itemsize, ctypes.byref(cfg._c()), self.rank,
+                                  self.world, self.ptrs, stream), "xpart_route")
+
+    def place(self, out_half):
+        """Passes 2 and 3 of this rank's buckets (after every rank's route finished)."""
+        import torch
+        stream = torch.cuda.current_stream(out_half.device).cuda_stream
+        check(lib.bsg_xpart_place(self.m, self.itemsize, self.rank, self.world, self.ptrs, out_half.data_ptr(),
+                                  stream), "xpart_place")
+
+    def shuffle(self, local_half, cfg: Optional[ShuffleConfig] = None, out=None):
+        """This rank's output half.  Host barriers order the passes across the pair: nobody appends into a
+        workspace (or resets its cursors) before its owner finished the previous place, and nobody places
+        before every rank's route completed."""
+        import torch
+        import torch.distributed as dist
+        cfg = cfg or ShuffleConfig()
+        if local_half.numel() * self.world != self.m or local_half.element_size() != self.itemsize:
+            raise _lib.InvalidArgument("exchange shuffle: local half of m elements of the workspace's type")
+        out = torch.empty_like(local_half) if out is None else out
+        torch.cuda.current_stream(local_half.device).synchronize()
+        dist.barrier(group=self.group)
+        self.route(local_half, cfg)
+        torch.cuda.current_stream(local_half.device).synchronize()
+        dist.barrier(group=self.group)
+        self.place(out)
+        return out
+
+    def close(self):
+        while self._opened:
+            check(lib.bsg_ipc_close(self._opened.pop()), "ipc_close")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

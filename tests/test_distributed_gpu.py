@@ -50,6 +50,17 @@ def _worker(rank, world, port, q):
         local = torch.arange(rank * S, (rank + 1) * S, dtype=torch.int64, device="cuda") * 7
         out = D.shuffle_values_sharded(local, m, bsg.ShuffleConfig(seed=5))
         res[("sharded", m)] = out.cpu().numpy().copy()
+        # exchange partition (bsg_xpart_*): input halves, peer stores into the owner's buckets, local P2/P3
+        for m, variant, dt, seed, rounds in (((1 << 20), 1, torch.int64, 11, 24), ((1 << 21), 0, torch.int32, 12, 24),
+                                             ((1 << 17), 1, torch.int64, 13, 7), ((1 << 22), 1, torch.int32, 14, 24)):
+            S = m // world
+            local = torch.arange(rank * S, (rank + 1) * S, dtype=dt, device="cuda") * 3 + 1
+            cfg = bsg.ShuffleConfig(seed=seed, variant=bsg.BijectionVariant(variant), num_rounds=rounds)
+            with D.ExchangeShuffle(m, dt) as X:
+                a = X.shuffle(local, cfg)
+                b = X.shuffle(local, cfg)  # reuse of the mapped workspaces
+                assert torch.equal(a, b)
+            res[("xpart", m)] = a.to(torch.int64).cpu().numpy().copy()
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -78,6 +89,11 @@ def test_two_ranks_on_one_gpu(orc):
     m = 1 << 20
     exp = orc.shuffle_values(np.arange(m, dtype=np.uint64) * 7, 5, 1, 24)
     assert np.array_equal(np.concatenate([out[r][("sharded", m)] for r in range(world)]).view(np.uint64), exp)
+    for m, variant, seed, rounds in (((1 << 20), 1, 11, 24), ((1 << 21), 0, 12, 24), ((1 << 17), 1, 13, 7),
+                                     ((1 << 22), 1, 14, 24)):
+        exp = orc.shuffle_indices(m, seed, variant, rounds) * np.uint64(3) + np.uint64(1)
+        got = np.concatenate([out[r][("xpart", m)] for r in range(world)]).view(np.uint64)
+        assert np.array_equal(got, exp), (m, variant, rounds)
 
 
 def _ipc_worker(rank, world, port, q):
