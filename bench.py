@@ -277,6 +277,7 @@ def ours_arm(args, rank, world, local, cpu=None):
     stream = torch.cuda.current_stream(dev)
     tdt = {4: torch.int32, 8: torch.int64, 16: torch.complex128}[eb]
 
+    xchg = False  # the two-rank exchange partition (set below for power-of-two domains at N = 2)
     if batch:
         m_total = m_gpu
         vals = torch.arange(m_gpu, dtype=tdt, device=dev).repeat(batch, 1)
@@ -292,7 +293,18 @@ def ours_arm(args, rank, world, local, cpu=None):
         # 16-byte records (C5) at N > 1: the input is SHARDED (rank r holds records [r*n, (r+1)*n)) and payload
         # reads go to peer HBM through CUDA-IPC mappings (NVLink); smaller payloads are replicated.
         sharded = eb == 16 and world > 1
-        if sharded:
+        pow2 = (m_total & (m_total - 1)) == 0
+        # Two ranks, power-of-two u32/u64 domain: the exchange partition (bsg_xpart_*) --
+        # rank r holds input half r, routes every element into its owner's buckets by peer stores and places its
+        # own output half.  BSG_BENCH_XPART=0 selects the counter-range single pass instead.
+        xchg = (world == 2 and pow2 and eb in (4, 8) and m_total <= (1 << 32)
+                and os.environ.get("BSG_BENCH_XPART", "1") == "1")
+        if xchg:
+            from paper_2106_06161_b200 import distributed as D
+            S = m_total // 2
+            vals = torch.arange(rank * S, (rank + 1) * S, dtype=tdt, device=dev)  # input half r (iota slice)
+            xpart = D.ExchangeShuffle(m_total, tdt, device=dev)
+        elif sharded:
             from paper_2106_06161_b200 import distributed as D
             vals = torch.arange(2 * rank * m_gpu, 2 * (rank + 1) * m_gpu, dtype=torch.int64,
                                 device=dev).view(torch.complex128)
@@ -300,7 +312,12 @@ def ours_arm(args, rank, world, local, cpu=None):
         else:
             vals = make_values(torch, m_total, eb, device=dev)  # replicated input
         step_bytes_rank = 2 * m_gpu * eb
-        if world == 1:
+        if xchg:
+            out = torch.empty(S, dtype=tdt, device=dev)
+
+            def step():
+                xpart.shuffle(vals, cfg, out)
+        elif world == 1:
             out = torch.empty(m_total, dtype=tdt, device=dev)
 
             def step():
@@ -323,9 +340,10 @@ def ours_arm(args, rank, world, local, cpu=None):
                                                       out.data_ptr(), eb, cnt_dev.data_ptr(),
                                                       stream.cuda_stream), "shuffle_range")
                 dist.all_gather_into_tensor(counts, cnt_dev)  # the 8-byte count exchange (NCCL)
-        pow2 = (m_total & (m_total - 1)) == 0
         partitioned = world == 1 and m_total * eb >= (256 << 20) and eb <= 8  # whole domain, >= 256 MiB
-        if partitioned:
+        if xchg:
+            dominant = "bsg::k_part1x+k_part2t+k_place"
+        elif partitioned:
             dominant = "bsg::k_part1+k_part2t+k_place" if pow2 else "bsg::k_part1+k_part2t+k_place_rank"
         elif not pow2:
             dominant = "bsg::k_compact_smem"
@@ -416,6 +434,8 @@ def ours_arm(args, rank, world, local, cpu=None):
     else:
         if world == 1:
             off_elems, n_elems = 0, m_total
+        elif xchg:
+            off_elems, n_elems = rank * S, S
         else:
             allc = [int(x) for x in counts.tolist()]
             off_elems, n_elems = sum(allc[:rank]), allc[rank]
@@ -501,6 +521,30 @@ def ours_arm(args, rank, world, local, cpu=None):
             sync = {"value": round(step_bytes_rank / (sync_ms * 1e-3) / 1e9, 3), "ms_per_step": round(sync_ms, 3),
                     "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call"}
             del pairs
+        elif xchg:
+            # each rank's host holds its input half: H2D, the exchange partition (route into the owners' buckets,
+            # barrier, place its own), D2H of its output half
+            host_in = vals.cpu().pin_memory()
+            host_out = torch.empty(S, dtype=tdt).pin_memory()
+
+            def e2e_step():
+                vals.copy_(host_in, non_blocking=True)
+                xpart.shuffle(vals, cfg, out)
+                host_out.copy_(out, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+            h2d, d2h = S * eb, S * eb
+            e2e_step()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                e2e_step()
+            barrier()
+            el = time.perf_counter() - t0
+            path = ("per rank: H2D of its input half, exchange partition (P1 stores into the owner rank's buckets "
+                    "through CUDA-IPC peer mappings, P2/P3 of its own buckets), D2H of its output half "
+                    "(distributed.ExchangeShuffle)")
+            sync = None
+            del host_in, host_out
         elif sharded:
             # each rank's host holds its input shard: H2D into the IPC-exported device shard, barrier, the
             # counter-range shuffle reading peers over NVLink, D2H of this rank's output piece
@@ -571,6 +615,8 @@ def ours_arm(args, rank, world, local, cpu=None):
             dist.barrier()
             if sharded_ipc is not None:
                 sharded_ipc.close()
+            if xchg:
+                xpart.close()
             dist.destroy_process_group()
 
     sharded_ipc = ipc if (not batch and sharded) else None
@@ -596,16 +642,20 @@ def ours_arm(args, rank, world, local, cpu=None):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPES[eb], "data": "synthetic (iota values, device-generated)",
         "config": {"workload": desc + ("" if world == 1 or batch else
-                                       f"; global shuffle of {world}x n elements, counter-range partition, "
-                                       + ("input sharded over the ranks, payload read from peer HBM via CUDA IPC"
-                                          if eb == 16 else "replicated input")),
+                                       f"; global shuffle of {world}x n elements, "
+                                       + ("exchange partition: input halves, P1 stores into the owner rank's "
+                                          "buckets through CUDA-IPC peer mappings, P2/P3 per rank" if xchg else
+                                          "counter-range partition, "
+                                          + ("input sharded over the ranks, payload read from peer HBM via CUDA IPC"
+                                             if eb == 16 else "replicated input"))),
                    "n_per_gpu": m_gpu, "n_total": m_total if not batch else batch * m_gpu * world,
                    "elem_bytes": eb, "seed": SEED, "rounds": 24,
                    "variant": "VariablePhilox" if variant else "Lcg",
                    "l2": (f"in+out {footprint / 2**20:.0f} MiB per step > 126 MB L2; no flush" if flush is None
                           else f"in+out {footprint / 2**20:.0f} MiB fits in L2: a 512 MiB buffer is written "
                                "between timed steps (each step timed alone)"),
-                   "parallelism": f"counter-range partition x{world}" if world > 1 else "single GPU"},
+                   "parallelism": ("exchange partition x2" if xchg else f"counter-range partition x{world}")
+                   if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 3), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kernel_ms, 4),

@@ -48,6 +48,23 @@ for cap in (8192, 0):  # windows above the staging cap: the list-driven k_place_
 rec = torch.arange(2 * (1 << 16), dtype=torch.int64, device="cuda").view(-1, 2)  # 16-byte records: k_part2t<uint4>
 got = bsg.shuffle_values(rec.view(torch.complex128), bsg.ShuffleConfig(seed=12)).view(torch.int64).view(-1, 2)
 check("partitioned 16-byte", got[:, 0].cpu().numpy().astype(np.uint64) // 2, O.shuffle_indices(1 << 16, 12))
+# two-rank exchange partition in one process (both workspaces local): k_part1x, k_xfill, P2 over regions, P3
+import ctypes
+from paper_2106_06161_b200._lib import check as _check, lib as _L
+for m, dt, eb in (((1 << 17), torch.int64, 8), ((1 << 18), torch.int32, 4)):
+    nb = ctypes.c_uint64()
+    _check(_L.bsg_xpart_workspace_bytes(m, eb, 2, ctypes.byref(nb)), "ws")
+    wsx = [torch.empty(nb.value, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    ptrs = (ctypes.c_void_p * 2)(wsx[0].data_ptr(), wsx[1].data_ptr())
+    xin = torch.arange(m, dtype=dt, device="cuda")
+    xout = torch.empty_like(xin)
+    st = torch.cuda.current_stream().cuda_stream
+    xc = bsg.ShuffleConfig(seed=21)._c()
+    for r in range(2):
+        _check(_L.bsg_xpart_route(xin[r * (m // 2):].data_ptr(), m, eb, ctypes.byref(xc), r, 2, ptrs, st), "route")
+    for r in range(2):
+        _check(_L.bsg_xpart_place(m, eb, r, 2, ptrs, xout[r * (m // 2):].data_ptr(), st), "place")
+    check(f"xpart {m}", xout.cpu().numpy().astype(np.uint64), O.shuffle_indices(m, 21))
 bsg.set_path(0)
 rows = torch.arange(1024, dtype=torch.int32, device="cuda").repeat(16, 1)
 out = bsg.shuffle_values_batched(rows, bsg.ShuffleConfig(seed=1000)).cpu().numpy()
