@@ -217,6 +217,10 @@ typedef struct bsg_pipeline bsg_pipeline;
 bsg_status bsg_pipeline_create(uint64_t max_m, uint32_t elem_bytes, int32_t depth, bsg_pipeline** out);
 bsg_status bsg_pipeline_submit(bsg_pipeline* p, const void* host_in, void* host_out, uint64_t m,
                                const bsg_config* cfg, uint64_t* ticket);
+/* Batched form (bsg_shuffle_values_batched, stats.hpp:314-324): batch rows of
+ * m elements, row b shuffled with seed + b; batch * m <= the pipeline's max_m. */
+bsg_status bsg_pipeline_submit_batched(bsg_pipeline* p, const void* host_in, void* host_out, uint64_t batch,
+                                       uint64_t m, const bsg_config* cfg, uint64_t* ticket);
 bsg_status bsg_pipeline_wait(bsg_pipeline* p, uint64_t ticket);
 bsg_status bsg_pipeline_destroy(bsg_pipeline* p);
 

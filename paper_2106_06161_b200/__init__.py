@@ -411,6 +411,21 @@ class Pipeline:
         self._keep[t.value] = (values, out)
         return t.value
 
+    def submit_batched(self, values: Any, out: Any, cfg: Optional[ShuffleConfig] = None) -> int:
+        """Rows of a 2-D host array, row b shuffled with seed + b (shuffle_values_batched), streamed."""
+        cfg = cfg or ShuffleConfig()
+        if len(values.shape) != 2 or tuple(out.shape) != tuple(values.shape):
+            raise InvalidArgument("pipeline: batched values must be 2-D (batch, m) and out of the same shape")
+        batch, m = int(values.shape[0]), int(values.shape[1])
+        vb, ob = _Buf(values), _Buf(out)
+        if vb.itemsize != self.elem_bytes or ob.itemsize != self.elem_bytes:
+            raise InvalidArgument("pipeline: element size mismatch")
+        t = ctypes.c_uint64()
+        check(lib.bsg_pipeline_submit_batched(self._h, vb.ptr, ob.ptr, batch, m, ctypes.byref(cfg._c()),
+                                              ctypes.byref(t)), "pipeline_submit_batched")
+        self._keep[t.value] = (values, out)
+        return t.value
+
     def wait(self, ticket: int) -> None:
         check(lib.bsg_pipeline_wait(self._h, ticket), "pipeline_wait")
         self._keep.pop(ticket, None)

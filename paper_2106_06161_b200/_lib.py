@@ -68,6 +68,8 @@ SIGNATURES = {
     "bsg_ipc_close": (c_int32, [c_void_p]),
     "bsg_pipeline_create": (c_int32, [c_uint64, c_uint32, c_int32, POINTER(c_void_p)]),
     "bsg_pipeline_submit": (c_int32, [c_void_p, c_void_p, c_void_p, c_uint64, POINTER(bsg_config), POINTER(c_uint64)]),
+    "bsg_pipeline_submit_batched": (c_int32, [c_void_p, c_void_p, c_void_p, c_uint64, c_uint64, POINTER(bsg_config),
+                                              POINTER(c_uint64)]),
     "bsg_pipeline_wait": (c_int32, [c_void_p, c_uint64]),
     "bsg_pipeline_destroy": (c_int32, [c_void_p]),
     "bsg_sort_shuffle_u64": (c_int32, [c_void_p, c_void_p, c_uint64, c_uint64, c_void_p]),

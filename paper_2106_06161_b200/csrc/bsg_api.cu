@@ -550,6 +550,36 @@ bsg_status bsg_shuffle_values(const void* in, void* out, uint64_t m, uint32_t el
   });
 }
 
+namespace {
+// Device part of bsg_shuffle_values_batched (device pointers, stream-ordered): row b shuffled with seed + b.
+bsg_status batched_device(DeviceCtx* c, const void* di, void* dO, uint64_t batch, uint64_t m, uint32_t elem_bytes,
+                          const bsg_config& cfg, cudaStream_t s) {
+  const int bits = bsg::domain_bits(m);
+  const int code = native_code(elem_bytes, di, dO);
+  if (m >= 3 && code > 0 && bsg::batched_supported(code, static_cast<uint32_t>(m), bits, cfg.num_rounds)) {
+    bsg::BatchedLaunch B;
+    B.in = di;
+    B.out = dO;
+    B.batch = batch;
+    B.m = static_cast<uint32_t>(m);
+    B.seed = cfg.seed;
+    BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, B.p));
+    BSG_TRY(ws_begin(c, s));
+    BSG_CUDA(bsg::launch_batched(code, B, s));
+    BSG_TRY(ws_end(c, s));
+    return BSG_OK;
+  }
+  const size_t row = m * static_cast<size_t>(elem_bytes);
+  for (uint64_t b = 0; b < batch; ++b) {
+    bsg_config cb = cfg;
+    cb.seed = cfg.seed + b;
+    BSG_TRY(shuffle_device(c, static_cast<const char*>(di) + b * row, static_cast<char*>(dO) + b * row, m,
+                           elem_bytes, cb, s));
+  }
+  return BSG_OK;
+}
+}  // namespace
+
 bsg_status bsg_shuffle_values_batched(const void* in, void* out, uint64_t batch, uint64_t m, uint32_t elem_bytes,
                                       const bsg_config* cfg_in, void* stream) {
   const bsg_config cfg = resolve_cfg(cfg_in);
@@ -579,27 +609,7 @@ bsg_status bsg_shuffle_values_batched(const void* in, void* out, uint64_t batch,
       BSG_CUDA(c->st_out.ensure(bytes));
       dO = c->st_out.p;
     }
-    const int code = native_code(elem_bytes, di, dO);
-    if (m >= 3 && code > 0 && bsg::batched_supported(code, static_cast<uint32_t>(m), bits, cfg.num_rounds)) {
-      bsg::BatchedLaunch B;
-      B.in = di;
-      B.out = dO;
-      B.batch = batch;
-      B.m = static_cast<uint32_t>(m);
-      B.seed = cfg.seed;
-      BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, B.p));
-      BSG_TRY(ws_begin(c, s));
-      BSG_CUDA(bsg::launch_batched(code, B, s));
-      BSG_TRY(ws_end(c, s));
-    } else {
-      const size_t row = m * static_cast<size_t>(elem_bytes);
-      for (uint64_t b = 0; b < batch; ++b) {
-        bsg_config cb = cfg;
-        cb.seed = cfg.seed + b;
-        BSG_TRY(shuffle_device(c, static_cast<const char*>(di) + b * row, static_cast<char*>(dO) + b * row, m,
-                               elem_bytes, cb, s));
-      }
-    }
+    BSG_TRY(batched_device(c, di, dO, batch, m, elem_bytes, cfg, s));
     if (!dout) BSG_CUDA(cudaMemcpyAsync(out, dO, bytes, cudaMemcpyDeviceToHost, s));
     if (!din || !dout) BSG_CUDA(cudaStreamSynchronize(s));
     return BSG_OK;
@@ -1053,6 +1063,37 @@ bsg_status bsg_pipeline_submit(bsg_pipeline* p, const void* host_in, void* host_
     BSG_TRY(shuffle_device(c, s.din.p, s.dout.p, m, p->eb, cfg, p->s_comp));
     BSG_CUDA(cudaEventRecord(s.kernel_done, p->s_comp));
     // D2H of the result.
+    BSG_CUDA(cudaStreamWaitEvent(p->s_d2h, s.kernel_done, 0));
+    BSG_CUDA(cudaMemcpyAsync(host_out, s.dout.p, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+    BSG_CUDA(cudaEventRecord(s.d2h_done, p->s_d2h));
+    return BSG_OK;
+  });
+}
+
+bsg_status bsg_pipeline_submit_batched(bsg_pipeline* p, const void* host_in, void* host_out, uint64_t batch,
+                                       uint64_t m, const bsg_config* cfg_in, uint64_t* ticket) {
+  if (!p) return fail(BSG_EINVAL, "pipeline: null handle");
+  if (batch != 0 && m > p->max_m / batch) return fail(BSG_EINVAL, "pipeline: batch * m exceeds the capacity");
+  if (host_in != nullptr && host_in == host_out) return fail(BSG_EALIAS, "shuffle_values_batched: out aliases input");
+  const bsg_config cfg = resolve_cfg(cfg_in);
+  if (m >= 3) {
+    BijParams bp;
+    BSG_TRY(build_params(cfg.variant, bsg::domain_bits(m), cfg.seed, cfg.num_rounds, bp));
+  }
+  const uint64_t t = p->next++;
+  auto& s = p->slots[t % p->slots.size()];
+  const size_t bytes = batch * m * static_cast<size_t>(p->eb);
+  if (ticket) *ticket = t;
+  s.ticket = t;
+  if (bytes == 0) return BSG_OK;
+  return with_ctx([&](DeviceCtx* c) -> bsg_status {
+    BSG_CUDA(cudaStreamWaitEvent(p->s_h2d, s.kernel_done, 0));
+    BSG_CUDA(cudaMemcpyAsync(s.din.p, host_in, bytes, cudaMemcpyHostToDevice, p->s_h2d));
+    BSG_CUDA(cudaEventRecord(s.h2d_done, p->s_h2d));
+    BSG_CUDA(cudaStreamWaitEvent(p->s_comp, s.h2d_done, 0));
+    BSG_CUDA(cudaStreamWaitEvent(p->s_comp, s.d2h_done, 0));
+    BSG_TRY(batched_device(c, s.din.p, s.dout.p, batch, m, p->eb, cfg, p->s_comp));
+    BSG_CUDA(cudaEventRecord(s.kernel_done, p->s_comp));
     BSG_CUDA(cudaStreamWaitEvent(p->s_d2h, s.kernel_done, 0));
     BSG_CUDA(cudaMemcpyAsync(host_out, s.dout.p, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
     BSG_CUDA(cudaEventRecord(s.d2h_done, p->s_d2h));

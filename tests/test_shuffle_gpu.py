@@ -396,6 +396,25 @@ def test_pipeline_streams_match_oracle(bsg, cuda):
             pipe.submit(pairs[0][0], pairs[0][1])  # m exceeds capacity
 
 
+def test_pipeline_batched_rows_match_oracle(bsg, cuda):
+    """bsg_pipeline_submit_batched: rows of pinned host buffers, row b shuffled with seed + b, streamed through
+    two slots (the C4 e2e path)."""
+    batch, m = 64, 1024
+    ins = [cuda.arange(m, dtype=cuda.int32).repeat(batch, 1).contiguous().pin_memory() for _ in range(3)]
+    outs = [cuda.empty(batch, m, dtype=cuda.int32).pin_memory() for _ in range(3)]
+    with bsg.Pipeline(batch * m, 4, depth=2) as pipe:
+        tickets = [pipe.submit_batched(ins[i], outs[i], cfg_of(bsg, seed=900 + 100 * i)) for i in range(3)]
+        for t in tickets:
+            pipe.wait(t)
+        with pytest.raises(bsg.InvalidArgument):
+            pipe.submit_batched(cuda.zeros(batch + 1, m, dtype=cuda.int32).pin_memory(),
+                                cuda.zeros(batch + 1, m, dtype=cuda.int32).pin_memory())  # exceeds capacity
+    for i in range(3):
+        for b in (0, 1, batch - 1):
+            exp = O.shuffle_indices(m, 900 + 100 * i + b)
+            assert np.array_equal(outs[i][b].numpy().astype(np.uint64), exp), (i, b)
+
+
 def test_partitioned_path_matches_single_pass(bsg, cuda, golden):
     """The three-pass partitioned kernel (pow2, large) is bit-identical to the fused single pass."""
     old = bsg.set_path(2)
