@@ -167,8 +167,9 @@ bsg_status bsg_dist_counter_range(uint64_t m, int32_t rank, int32_t world, uint6
  * bsg_xpart_workspace_bytes of device memory, maps its peer's workspace
  * (bsg_ipc_export/open) and passes both as workspaces[0..1] (rank order).
  * bsg_xpart_route streams the rank's input half through the inverse cipher
- * and appends every element to its destination bucket's region in the owner
- * rank's workspace (peer stores over NVLink, no remote atomics).  After BOTH
+ * and appends every element to its destination bucket in the owner rank's
+ * workspace, rank 0 from the front and rank 1 from the back (peer stores over
+ * NVLink, no remote atomics).  After BOTH
  * ranks' route completed (host barrier), bsg_xpart_place partitions and
  * places the rank's own buckets into out_half.  Device pointers; both calls
  * asynchronous on `stream`. */

@@ -458,8 +458,7 @@ template <typename T, int TILE = kP2Tile>
 __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                        T* __restrict__ ov, uint16_t* __restrict__ od,
                                                        uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
-                                                       uint32_t ntiles, const uint32_t* __restrict__ cnt1,
-                                                       int rsh = 0) {
+                                                       uint32_t ntiles, const uint32_t* __restrict__ cnt1) {
   constexpr int kItems = TILE / kP2Threads, kTileLog = __builtin_ctz(TILE);
   extern __shared__ __align__(16) unsigned char smem[];
   T* gv = reinterpret_cast<T*>(smem);                    // staging: values of the next tile
@@ -502,7 +501,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
   for (; t < ntiles; phase ^= 1) {
     mbar_wait(&bar, phase);
     const uint32_t nv = fill(t), tn = next(t + gridDim.x);
-    const uint64_t coarse = (t >> tpblog) >> rsh;  // rsh: 2^rsh regions per coarse bucket (exchange path)
+    const uint64_t coarse = t >> tpblog;
     uint32_t d[kItems], rk[kItems];
 #ifndef BSG_P2T_EARLY
 #define BSG_P2T_EARLY 1
@@ -1210,11 +1209,11 @@ cudaError_t dispatch_partition(const PartitionLaunch& a, cudaStream_t s) {
 // Exchange partition (two ranks, power-of-two domain of 2^G counters, input sharded in two halves): the
 // partitioned path with its first pass writing across the pair.  Rank r streams its input half (global indices
 // j = r * 2^(G-1) + i), computes f^-1(j) once per element and counting-sorts each tile into the 2 * 2^s1 coarse
-// buckets of the GLOBAL domain; buckets [0, 2^s1) are rank 0's output half, the rest rank 1's.  A bucket's
-// owner holds one region per source rank (capacity = the bucket span, so no count pass is needed), and the
-// source appends to its own region with its own cursors: peer traffic is plain stores (NVLink) with no remote
-// atomics.  After both ranks' P1, each owner reads the two sources' cursors as region fills and runs P2 (regions
-// of one bucket share its window cursors) and P3 on its own 2^(G-1) outputs.  The output half of rank r is
+// buckets of the GLOBAL domain; buckets [0, 2^s1) are rank 0's output half, the rest rank 1's.  Every bucket
+// receives exactly its span of elements from the two sources together (a power-of-two domain has no padding),
+// so source 0 fills its buckets from the front and source 1 from the back, each with its own cursors: peer
+// traffic is plain stores (NVLink) with no remote atomics, and the buckets end up exactly full -- the owner's
+// P2 and P3 are the single-GPU passes over its 2^(G-1) outputs.  The output half of rank r is
 // out[r * 2^(G-1), (r + 1) * 2^(G-1)) of the single-GPU shuffle of all 2^G elements.
 namespace {
 template <int KIND, int D, typename T>
@@ -1248,9 +1247,11 @@ __global__ void __launch_bounds__(kP1Threads, p1_f64<KIND, D>() ? BSG_P1_MINB_F6
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = tid + k * kP1Threads;
-    // region (bucket i within its owner, source) of capacity 2^bshift in the owner's arrays
-    if (i < nb) delta[i] = ((((static_cast<uint32_t>(i) & ((1u << s1) - 1u)) << 1) | static_cast<uint32_t>(src))
-                            << bshift) + g[k] - start[i];  // mod 2^32
+    // bucket i within its owner: source 0 appends from the front, source 1 from the back (run [cap - g - n, cap - g))
+    if (i < nb) {
+      const uint32_t b0 = (static_cast<uint32_t>(i) & ((1u << s1) - 1u)) << bshift;
+      delta[i] = (src ? b0 + (1u << bshift) - g[k] - hist[i] : b0 + g[k]) - start[i];  // mod 2^32
+    }
   }
   __syncthreads();  // start[] read for delta before the rank atomics advance it
 #pragma unroll
@@ -1271,19 +1272,9 @@ __global__ void __launch_bounds__(kP1Threads, p1_f64<KIND, D>() ? BSG_P1_MINB_F6
   }
 }
 
-// Region fills of the owner's buckets: region (b, src) holds the count source src appended to global bucket
-// owner * 2^s1 + b (that source's cursor, read from its workspace -- a peer mapping for the other rank).
-__global__ void k_xfill(const uint32_t* __restrict__ cur_src0, const uint32_t* __restrict__ cur_src1,
-                        uint32_t* __restrict__ cnt1, int s1, int owner) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= (2 << s1)) return;
-  const int b = (owner << s1) + (q >> 1);
-  cnt1[q] = (q & 1) ? cur_src1[b] : cur_src0[b];
-}
-
 struct XLayout {
   int G, Lb, w2, s1, s2;
-  size_t tv, td, dlow, cur, cur2, cnt1, total;
+  size_t tv, td, dlow, cur, cur2, total;
 };
 XLayout xlayout(int elem_code, int G) {
   XLayout L{};
@@ -1291,7 +1282,7 @@ XLayout xlayout(int elem_code, int G) {
   L.Lb = G - 1;
   L.w2 = elem_code == 4 ? 14 : 13;
   part_split(L.Lb, L.w2, L.s1, L.s2);
-  const uint64_t R = 2ULL << L.Lb;  // region slots: two sources per bucket
+  const uint64_t R = 1ULL << L.Lb;  // the owner's buckets, exactly full
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   size_t o = 0;
   L.tv = o;
@@ -1304,8 +1295,6 @@ XLayout xlayout(int elem_code, int G) {
   o = al(o + (2u << L.s1) * 4);
   L.cur2 = o;
   o = al(o + (static_cast<size_t>(1) << (L.s1 + L.s2)) * 4);
-  L.cnt1 = o;
-  o = al(o + (2u << L.s1) * 4);
   L.total = o;
   return L;
 }
@@ -1343,13 +1332,9 @@ template <typename T>
 cudaError_t run_xplace(const XpartLaunch& a, cudaStream_t s) {
   const XLayout L = xlayout(sizeof(T), a.G);
   char* me = static_cast<char*>(a.ws[a.rank]);
-  uint32_t* cnt1 = reinterpret_cast<uint32_t*>(me + L.cnt1);
   uint32_t* cur2 = reinterpret_cast<uint32_t*>(me + L.cur2);
   cudaError_t e = cudaMemsetAsync(cur2, 0, (static_cast<size_t>(1) << (L.s1 + L.s2)) * 4, s);
   if (e != cudaSuccess) return e;
-  k_xfill<<<((2 << L.s1) + 255) / 256, 256, 0, s>>>(
-      reinterpret_cast<const uint32_t*>(static_cast<char*>(a.ws[0]) + L.cur),
-      reinterpret_cast<const uint32_t*>(static_cast<char*>(a.ws[1]) + L.cur), cnt1, L.s1, a.rank);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1358,17 +1343,17 @@ cudaError_t run_xplace(const XpartLaunch& a, cudaStream_t s) {
   int per = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T, kP2Tile>, kP2Threads, smt);
   const uint64_t w1 = 1ULL << (L.Lb - L.s1);
-  const uint64_t tiles = (2ULL << L.Lb) / kP2Tile;  // region tile slots (two regions per bucket)
+  const uint64_t tiles = (1ULL << L.Lb) / kP2Tile;
   const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
   uint16_t* dlow = reinterpret_cast<uint16_t*>(me + L.dlow);
   k_part2t<T, kP2Tile><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
       reinterpret_cast<const T*>(me + L.tv), reinterpret_cast<const uint32_t*>(me + L.td), static_cast<T*>(a.out),
-      dlow, cur2, L.w2, 1 << L.s2, w1, static_cast<uint32_t>(tiles), cnt1, 1);
+      dlow, cur2, L.w2, 1 << L.s2, w1, static_cast<uint32_t>(tiles), nullptr);
   const size_t sm3 = (size_t{1} << L.w2) * sizeof(T);
   cudaFuncSetAttribute(k_place<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
   k_place<T><<<static_cast<unsigned>((1ULL << L.Lb) >> L.w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), dlow,
                                                                                     L.w2, g_bulk_stores);
-  note_launch(3);
+  note_launch(2);
   return cudaGetLastError();
 }
 

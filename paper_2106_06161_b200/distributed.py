@@ -232,9 +232,10 @@ def ipc_shards(local_shard, group=None) -> IpcShards:
 class ExchangeShuffle:
     """Two-rank exchange-partitioned shuffle of a power-of-two domain sharded in halves (bsg_xpart_*, DESIGN.md
     section 7): rank r holds input elements and output positions [r*m/2, (r+1)*m/2).  Each rank streams its input
-    half through the inverse cipher once and appends every element to its destination bucket's region in the
-    owner rank's workspace (peer stores through a CUDA-IPC mapping, NVLink between GPUs, no remote atomics); then
-    each rank partitions and places its own buckets.  The concatenated halves equal the single-GPU shuffle.
+    half through the inverse cipher once and appends every element to its destination bucket in the owner rank's
+    workspace -- rank 0 from the bucket's front, rank 1 from its back, so the buckets end up exactly full (peer
+    stores through a CUDA-IPC mapping, NVLink between GPUs, no remote atomics); then each rank partitions and
+    places its own buckets.  The concatenated halves equal the single-GPU shuffle.
     The workspaces are allocated and mapped once (m and the element type fixed); `close()` unmaps the peer's."""
 
     def __init__(self, m: int, dtype, group=None, device=None):
