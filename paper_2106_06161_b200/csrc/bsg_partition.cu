@@ -1282,6 +1282,11 @@ XLayout xlayout(int elem_code, int G) {
   L.Lb = G - 1;
   L.w2 = elem_code == 4 ? 14 : 13;
   part_split(L.Lb, L.w2, L.s1, L.s2);
+  // P1 sorts into both ranks' buckets (2 << s1 <= kMaxB1): move a coarse bit to the fine split if needed
+  while ((2 << L.s1) > kMaxB1 && L.s1 > 1) {
+    --L.s1;
+    ++L.s2;
+  }
   const uint64_t R = 1ULL << L.Lb;  // the owner's buckets, exactly full
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   size_t o = 0;

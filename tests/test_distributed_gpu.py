@@ -166,3 +166,58 @@ def test_ipc_sharded_ranks_on_one_gpu(orc, world):
             off, piece = out[r][(m, variant, eb)]
             full[off * k:off * k + len(piece)] = piece.view(np.uint64)
         assert np.array_equal(full, exp), (world, m, variant, eb)
+
+
+def _xpart_max_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_06161_b200 as bsg
+    from paper_2106_06161_b200 import distributed as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = 1 << 32  # the largest exchange domain: 32-bit global indices and bucket positions
+        S = m // world
+        local = torch.arange(rank * S, (rank + 1) * S, dtype=torch.int64, device="cuda").to(torch.int32)
+        with D.ExchangeShuffle(m, torch.int32) as X:
+            out = X.shuffle(local, bsg.ShuffleConfig(seed=77))
+        del local
+        pieces = {}
+        for c0 in (0, S - 4096, S, m - 4096):  # head, both sides of the rank boundary, tail
+            if rank * S <= c0 < (rank + 1) * S:
+                pieces[c0] = out[c0 - rank * S:c0 - rank * S + 4096].to(torch.int64).cpu().numpy() & 0xFFFFFFFF
+        q.put((rank, pieces))
+        del out
+        torch.cuda.empty_cache()
+    except BaseException as e:  # report instead of leaving the parent waiting on the queue
+        q.put((rank, {"error": repr(e)}))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_partition_full_32_bit_domain(orc):
+    """bsg_xpart_* at m = 2^32 u32 (each rank 2^31 elements): global indices, bucket positions and the front/back
+    fills at the top of the 32-bit range; slices of the output against the oracle's counter-range images."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_xpart_max_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(world):
+        got.update(q.get(timeout=900)[1])
+        assert "error" not in got, got.get("error")
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    m = 1 << 32
+    for c0, piece in sorted(got.items()):
+        exp = orc.shuffle_indices_range(m, 77, 1, 24, c0, c0 + 4096)
+        assert np.array_equal(piece.astype(np.uint64), exp), c0
