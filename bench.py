@@ -538,7 +538,8 @@ def ours_arm(args, rank, world, local, cpu=None):
                     f"shuffle kernels, D2H of n*{eb} B to pinned host memory; 3 streams, 2 device slots, so step "
                     "i+1's H2D overlaps step i's D2H")
             sync = {"value": round(step_bytes_rank / (sync_ms * 1e-3) / 1e9, 3), "ms_per_step": round(sync_ms, 3),
-                    "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call"}
+                    "path": "bsg_shuffle_values(host pinned in, host pinned out), synchronous per call (partitioned path: "
+                            "its H2D chunked under P1, its D2H under P3)"}
             del pairs
         elif xchg:
             # each rank's host holds its input half: H2D, the exchange partition (route into the owners' buckets,

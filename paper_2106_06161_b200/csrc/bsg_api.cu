@@ -100,8 +100,20 @@ struct DeviceCtx {
   DevBuf part;                           // partitioned-path workspace
   std::deque<std::vector<uint32_t>> captured_keys;  // host key schedules read by captured graphs
   cudaEvent_t ws_done = nullptr;
+  // staged host-pointer calls: copy streams and events of the chunked H2D / D2H (created on first use)
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  std::vector<cudaEvent_t> stage_ev;
   bool ready = false;
 };
+
+// Host buffers a synchronous host-pointer call hands to run_range: the partitioned path overlaps their copies
+// with its first and last passes (chunks); any other path copies them whole around the kernel on the stream.
+struct StageIO {
+  const void* h_in = nullptr;
+  void* h_out = nullptr;
+  size_t in_bytes = 0, out_bytes = 0;
+};
+constexpr int kStageChunks = 8;
 
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
@@ -268,8 +280,20 @@ int native_code(uint32_t eb, const void* a, const void* b) {
 
 // Device-pointer core: range [c0, c1) of an m >= 3 shuffle.  elem_code 0 =
 // indices.  count_dev (device) receives the survivor count when non-null.
+bsg_status stage_streams(DeviceCtx* c) {
+  if (!c->cs_in) BSG_CUDA(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking));
+  if (!c->cs_out) BSG_CUDA(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
+  while (c->stage_ev.size() < 2 * kStageChunks + 2) {
+    cudaEvent_t e;
+    BSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->stage_ev.push_back(e);
+  }
+  return BSG_OK;
+}
+
 bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c0, uint64_t c1, const bsg::Src& src,
-                     void* out, int elem_code, unsigned long long* count_dev, cudaStream_t s) {
+                     void* out, int elem_code, unsigned long long* count_dev, cudaStream_t s,
+                     const StageIO* io = nullptr) {
   const int bits = bsg::domain_bits(m);
   BijParams p;
   BSG_TRY(build_params(cfg.variant, bits, cfg.seed, cfg.num_rounds, p));
@@ -294,7 +318,18 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
       P.out = out;
       P.m = m;
       P.p = p;
+      if (io) {
+        BSG_TRY(stage_streams(c));
+        P.h_in = io->h_in;
+        P.h_out = pow2 ? io->h_out : nullptr;  // padded outputs leave by one copy after the rank placement
+        P.cs_in = c->cs_in;
+        P.cs_out = c->cs_out;
+        P.ev = c->stage_ev.data();
+        P.chunks = kStageChunks;
+      }
       BSG_CUDA(bsg::launch_partition(elem_code, P, s));
+      if (io && io->h_out && !P.h_out)
+        BSG_CUDA(cudaMemcpyAsync(io->h_out, out, io->out_bytes, cudaMemcpyDeviceToHost, s));
       if (count_dev) BSG_CUDA(bsg::launch_store_u64(count_dev, m, s));
       return ws_end(c, s);
     }
@@ -313,7 +348,10 @@ bsg_status run_range(DeviceCtx* c, uint64_t m, const bsg_config& cfg, uint64_t c
     const uint64_t tile = bsg::kCompactTileMin;  // sizes the status words for the smallest tile
     BSG_TRY(lookback_prepare(c, (c1 - c0 + tile - 1) / tile, s, L.lb));
   }
+  if (io && io->h_in)
+    BSG_CUDA(cudaMemcpyAsync(const_cast<void*>(src.base), io->h_in, io->in_bytes, cudaMemcpyHostToDevice, s));
   if (c1 > c0) BSG_CUDA(bsg::launch_shuffle(elem_code, L, s));
+  if (io && io->h_out) BSG_CUDA(cudaMemcpyAsync(io->h_out, out, io->out_bytes, cudaMemcpyDeviceToHost, s));
   if (count_dev && (!L.compact || c1 == c0)) BSG_CUDA(bsg::launch_store_u64(count_dev, c1 - c0, s));
   return ws_end(c, s);
 }
@@ -534,6 +572,21 @@ bsg_status bsg_shuffle_values(const void* in, void* out, uint64_t m, uint32_t el
     const void* di = in;
     void* dO = out;
     BSG_TRY(ws_begin(c, s));  // order the staging writes after earlier asynchronous users of st_*
+    const int code = native_code(elem_bytes, in, out);
+    if (!din && !dout && m >= 3 && code > 0) {
+      // both buffers on the host: the copies travel with the shuffle (chunked under the partitioned passes)
+      BSG_CUDA(c->st_in.ensure(bytes));
+      BSG_CUDA(c->st_out.ensure(bytes));
+      StageIO io;
+      io.h_in = in;
+      io.h_out = out;
+      io.in_bytes = io.out_bytes = bytes;
+      bsg::Src src;
+      src.base = c->st_in.p;
+      BSG_TRY(run_range(c, m, cfg, 0, 1ULL << bsg::domain_bits(m), src, c->st_out.p, code, nullptr, s, &io));
+      BSG_CUDA(cudaStreamSynchronize(s));
+      return BSG_OK;
+    }
     if (!din) {
       BSG_CUDA(c->st_in.ensure(bytes));
       BSG_CUDA(cudaMemcpyAsync(c->st_in.p, in, bytes, cudaMemcpyHostToDevice, s));

@@ -602,12 +602,12 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // P3: place each fine window through shared memory, in place in `out`.
 template <typename T>
 __global__ void __launch_bounds__(kP3Threads) k_place(T* __restrict__ out, uint16_t* __restrict__ od, int w2,
-                                                      int bulk) {
+                                                      int bulk, uint32_t w0 = 0) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* win = reinterpret_cast<T*>(smem);
   const uint32_t W = 1u << w2;
-  T* o = out + (static_cast<uint64_t>(blockIdx.x) << w2);
-  const uint16_t* dd = od + (static_cast<uint64_t>(blockIdx.x) << w2);
+  T* o = out + (static_cast<uint64_t>(w0 + blockIdx.x) << w2);  // w0: first window of a staged chunk
+  const uint16_t* dd = od + (static_cast<uint64_t>(w0 + blockIdx.x) << w2);
   constexpr int kU = 8;
   for (uint32_t i0 = threadIdx.x; i0 < W; i0 += kP3Threads * kU) {
     T v[kU];
@@ -1075,6 +1075,12 @@ void part_split(int bits, int w2, int& s1, int& s2, bool pad = false) {
   s2 = total - s1;
 }
 
+#define BSG_STAGE_CHECK(x)                 \
+  do {                                     \
+    const cudaError_t e_ = (x);            \
+    if (e_ != cudaSuccess) return e_;      \
+  } while (0)
+
 template <int KIND, int D, typename T>
 cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   const int b = a.p.bits;
@@ -1112,7 +1118,31 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   // view x[1:] of a u64 tensor) takes the register-loading k_part1.
   const bool in_aligned = (reinterpret_cast<uintptr_t>(a.in) & 15u) == 0;
   uint64_t done1 = 0;
-  if (kTmaP1 && in_aligned && full1 > 0 && nb1 <= 256) {
+  const bool staged = a.h_in != nullptr;
+  if (staged) {
+    // Host input: copy it in chunks of whole tiles on the copy stream and let each chunk's P1 start as soon as its
+    // bytes landed, so the inverse cipher runs under the rest of the H2D (the synchronous host-pointer call).
+    BSG_STAGE_CHECK(cudaEventRecord(a.ev[0], s));  // the copies follow earlier work on s (staging reuse)
+    BSG_STAGE_CHECK(cudaStreamWaitEvent(a.cs_in, a.ev[0], 0));
+    const int K = a.chunks;
+    for (int k = 0; k < K; ++k) {
+      const uint64_t t0 = tiles1 * k / K, t1 = tiles1 * (k + 1) / K;
+      if (t1 == t0) continue;
+      const uint64_t e0 = t0 * kP1Tile, e1 = std::min<uint64_t>(t1 * kP1Tile, m);
+      BSG_STAGE_CHECK(cudaMemcpyAsync(const_cast<T*>(static_cast<const T*>(a.in)) + e0,
+                                      static_cast<const T*>(a.h_in) + e0, (e1 - e0) * sizeof(T),
+                                      cudaMemcpyHostToDevice, a.cs_in));
+      BSG_STAGE_CHECK(cudaEventRecord(a.ev[1 + k], a.cs_in));
+      BSG_STAGE_CHECK(cudaStreamWaitEvent(s, a.ev[1 + k], 0));
+      const uint64_t tf = std::min<uint64_t>(t1, full1);  // full tiles of this chunk
+      if (tf > t0)
+        k_part1<KIND, D, T, false><<<static_cast<unsigned>(tf - t0), kP1Threads, sm1, s>>>(
+            static_cast<const T*>(a.in), tv, a.tmp_dest, cur1, a.p, b - s1, nb1, w1, a.dest_in, m,
+            static_cast<uint32_t>(t0));
+    }
+    done1 = full1;
+  }
+  if (!staged && kTmaP1 && in_aligned && full1 > 0 && nb1 <= 256) {
     const size_t smt = kP1Tile * (2 * sizeof(T) + 4);
     cudaFuncSetAttribute(k_part1t<KIND, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
     int per = 1;
@@ -1183,6 +1213,26 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   } else if (!BSG_P2T16) {
     k_part2<T><<<static_cast<unsigned>(n / kP2Tile), kP2Threads, sm2, s>>>(tv, a.tmp_dest, static_cast<T*>(a.out),
                                                                             a.tmp_dlow, cur2, w2, nb2, w1);
+  }
+  if (a.h_out) {
+    // Host output: place the windows in chunks and copy each chunk out on the copy stream while the next is placed;
+    // s finally waits for the last copy, so a caller that synchronises s has the whole output.
+    const uint64_t nw = n >> w2;
+    const int K = a.chunks;
+    for (int k = 0; k < K; ++k) {
+      const uint64_t q0 = nw * k / K, q1 = nw * (k + 1) / K;
+      if (q1 == q0) continue;
+      k_place<T><<<static_cast<unsigned>(q1 - q0), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2,
+                                                                          g_bulk_stores, static_cast<uint32_t>(q0));
+      BSG_STAGE_CHECK(cudaEventRecord(a.ev[1 + K + k], s));
+      BSG_STAGE_CHECK(cudaStreamWaitEvent(a.cs_out, a.ev[1 + K + k], 0));
+      BSG_STAGE_CHECK(cudaMemcpyAsync(static_cast<T*>(a.h_out) + (q0 << w2), static_cast<T*>(a.out) + (q0 << w2),
+                                      ((q1 - q0) << w2) * sizeof(T), cudaMemcpyDeviceToHost, a.cs_out));
+    }
+    BSG_STAGE_CHECK(cudaEventRecord(a.ev[1 + 2 * K], a.cs_out));
+    BSG_STAGE_CHECK(cudaStreamWaitEvent(s, a.ev[1 + 2 * K], 0));
+    note_launch(3);
+    return cudaGetLastError();
   }
   k_place<T><<<static_cast<unsigned>(n >> w2), kP3Threads, sm3, s>>>(static_cast<T*>(a.out), a.tmp_dlow, w2,
                                                                        g_bulk_stores);

@@ -22,6 +22,14 @@ struct PartitionLaunch {
   void* tmp_values2 = nullptr;     // n * elem bytes
   uint32_t* win_prefix = nullptr;  // n >> window_log2 words
   uint32_t* win_list = nullptr;    // windows left to the round-based last pass (count at cursors[kCursorWords])
+  // Staged host buffers (synchronous host-pointer calls): h_in is copied into `in` chunk by chunk on cs_in with
+  // P1 following each chunk; h_out (power-of-two domains) receives `out` chunk by chunk on cs_out as P3 places
+  // it.  ev holds 2 * chunks + 2 events.
+  const void* h_in = nullptr;
+  void* h_out = nullptr;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t* ev = nullptr;
+  int chunks = 0;
 };
 
 struct RouteLaunch {

@@ -702,6 +702,26 @@ def test_partitioned_non_power_of_two_overflow_windows(bsg, cuda):
         bsg.set_path(old_path)
 
 
+def test_partitioned_host_buffers_staged(bsg, cuda):
+    """Host input and output through the partitioned path: the H2D is chunked under P1 and (power of two) the D2H
+    under P3 (StageIO in bsg_shuffle_values); pinned and pageable buffers, both bijections, padded domains."""
+    old = bsg.set_path(2)
+    try:
+        for m, variant, dt, pinned in [((1 << 20), PHILOX, cuda.int64, True), ((1 << 20) + 3, PHILOX, cuda.int64, True),
+                                       ((1 << 21), LCG, cuda.int32, False), ((1 << 19) + 77, LCG, cuda.int32, True),
+                                       (12345, PHILOX, cuda.int64, False)]:
+            vals = cuda.arange(m, dtype=dt) * 3 + 1
+            out = cuda.empty_like(vals)
+            if pinned:
+                vals, out = vals.pin_memory(), out.pin_memory()
+            bsg.shuffle_values_into(vals, cfg_of(bsg, seed=m, variant=variant), out)
+            got = out.numpy().astype(np.int64).view(np.uint64)
+            exp = O.shuffle_indices(m, m, variant, 24) * np.uint64(3) + np.uint64(1)
+            assert np.array_equal(got, exp), (m, variant, dt, pinned)
+    finally:
+        bsg.set_path(old)
+
+
 def test_partitioned_bulk_and_plain_stores_agree(bsg, cuda):
     """The last passes write placed windows by bulk shared->global copies (default) or plain stores
     (bsg_set_bulk_stores(0)): both equal the oracle, power of two or padded, aligned or not."""
