@@ -45,6 +45,9 @@ for cap in (8192, 0):  # windows above the staging cap: the list-driven k_place_
     check(f"partitioned padded cap {cap}", bsg.shuffle_values(vals, bsg.ShuffleConfig(seed=11)).cpu().numpy().view(np.uint64),
           O.shuffle_indices(m, 11))
     bsg.set_rank_stage_cap(old_cap)
+for m in ((1 << 16), (1 << 16) + 9):  # host buffers: chunked H2D under P1, chunked D2H under P3 (StageIO)
+    hv = np.arange(m, dtype=np.uint64)
+    check(f"partitioned host staged {m}", bsg.shuffle_values(hv, bsg.ShuffleConfig(seed=13)), O.shuffle_indices(m, 13))
 rec = torch.arange(2 * (1 << 16), dtype=torch.int64, device="cuda").view(-1, 2)  # 16-byte records: k_part2t<uint4>
 got = bsg.shuffle_values(rec.view(torch.complex128), bsg.ShuffleConfig(seed=12)).view(torch.int64).view(-1, 2)
 check("partitioned 16-byte", got[:, 0].cpu().numpy().astype(np.uint64) // 2, O.shuffle_indices(1 << 16, 12))
