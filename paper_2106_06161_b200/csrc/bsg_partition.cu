@@ -200,12 +200,14 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) > 8 ? 2 : (p1_f64<KIND, 
 #ifndef BSG_P1_LATE_LOAD
 #define BSG_P1_LATE_LOAD 1
 #endif
-  // LATE_LOAD (default): the values stay out of registers during the cipher (80 registers, 3 CTAs/SM) and are
-  // loaded straight into their sorted slots after the scan; 0 loads them first so their latency hides under the
-  // cipher (103 registers, 2 CTAs/SM; measured 1.5% slower for C2).
-  T v[BSG_P1_LATE_LOAD ? 1 : kP1Items];
+  // Late loads (the 3-CTA/SM IMAD.HI form): the values stay out of registers during the cipher (80 registers) and
+  // are loaded straight into their sorted slots after the scan.  The FP64-cipher form runs at 2 CTAs/SM anyway, so
+  // it loads them first and their latency hides under the cipher (108 registers; C2 P1 3.71 -> 3.60 ms, shuffle
+  // 7.59 -> 7.42 ms; the IMAD.HI form is neutral either way).
+  constexpr bool kLate = BSG_P1_LATE_LOAD && !p1_f64<KIND, D>();
+  T v[kLate ? 1 : kP1Items];
   auto valid = [&](int i) { return !PAD || tid + i * kP1Threads < static_cast<int>(nvalid); };
-  if constexpr (!BSG_P1_LATE_LOAD) {
+  if constexpr (!kLate) {
 #pragma unroll
     for (int i = 0; i < kP1Items; ++i)
       if (valid(i)) v[i] = __ldcs(in + base + i * kP1Threads);
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) > 8 ? 2 : (p1_f64<KIND, 
     for (int i = 0; i < kP1Items; ++i) {
       if (!valid(i)) continue;
       const uint32_t r = atomicAdd(&start[dst[i] >> bshift], 1u);
-      if constexpr (BSG_P1_LATE_LOAD) sv[r] = __ldcs(in + base + i * kP1Threads);
+      if constexpr (kLate) sv[r] = __ldcs(in + base + i * kP1Threads);
       else sv[r] = v[i];
       sd[r] = dst[i];
     }
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(kP1Threads, sizeof(T) > 8 ? 2 : (p1_f64<KIND, 
 #pragma unroll
     for (int i = 0; i < kP1Items; ++i) {
       if (!valid(i)) continue;
-      if constexpr (BSG_P1_LATE_LOAD) sv[rk[i]] = __ldcs(in + base + i * kP1Threads);
+      if constexpr (kLate) sv[rk[i]] = __ldcs(in + base + i * kP1Threads);
       else sv[rk[i]] = v[i];
       sd[rk[i]] = dst[i];
     }
