@@ -470,7 +470,10 @@ def ours_arm(args, rank, world, local, cpu=None):
         bcfg = bsg.ShuffleConfig(seed=SEED + rank * batch, variant=cfg.variant)
         nb = batch * m_gpu * eb
         # headline: the streaming C-ABI (bsg_pipeline_submit_batched): step i+1's H2D overlaps step i's D2H;
-        # each step is a full batch of shuffles whose result lands in its own pinned host buffer
+        # each step is a full batch of shuffles whose result lands in its own pinned host buffer.  A batch moves
+        # only 2 x 32 MiB, so the stream runs at least 40 steps (~40 ms) for the pipeline's fill and drain (one
+        # H2D and one D2H alone) to be paid once per job rather than dominate it.
+        e2e_steps = max(e2e_steps, 40)
         outs = [torch.empty_like(host_in).pin_memory() for _ in range(2)]
         with bsg.Pipeline(batch * m_gpu, eb, depth=2) as pl:
             pl.wait(pl.submit_batched(host_in, outs[0], bcfg))
