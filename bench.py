@@ -515,6 +515,8 @@ def ours_arm(args, rank, world, local, cpu=None):
             pairs = [(make_values(torch, m_total, eb, pin=True), torch.empty(m_total, dtype=tdt).pin_memory())
                      for _ in range(1 if eb == 16 else 2)]
             h2d, d2h = m_total * eb, m_total * eb
+            if h2d < (256 << 20):
+                e2e_steps = max(e2e_steps, 40)  # small steps (C1): pay the pipeline's fill and drain once per job
             with bsg.Pipeline(m_total, eb, depth=2) as pipe:
                 P = len(pairs)
                 tk = [pipe.submit(pairs[i % P][0], pairs[i % P][1], cfg) for i in range(2)]  # warm-up
