@@ -456,7 +456,11 @@ __global__ void __launch_bounds__(kP2Threads, sizeof(T) <= 8 ? 3 : 2)
 // loads leaves the per-tile critical path.
 // cnt1 != nullptr (non-power-of-two domains): coarse bucket b holds cnt1[b] <= w1 elements, so tile k of the
 // bucket is partial or empty; empty tiles are skipped before their loads are issued.
-template <typename T, int TILE = kP2Tile>
+// PAD = false (power-of-two domains): every tile is full, so the per-element bounds checks compile away.
+#ifndef BSG_P2_FULLT
+#define BSG_P2_FULLT 1
+#endif
+template <typename T, int TILE = kP2Tile, bool PAD = true>
 __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv, const uint32_t* __restrict__ td,
                                                        T* __restrict__ ov, uint16_t* __restrict__ od,
                                                        uint32_t* __restrict__ cur2, int w2, int nb2, uint64_t w1,
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
   if (tid == 0 && t < ntiles) issue(t);
   for (; t < ntiles; phase ^= 1) {
     mbar_wait(&bar, phase);
-    const uint32_t nv = fill(t), tn = next(t + gridDim.x);
+    const uint32_t nv = PAD ? fill(t) : static_cast<uint32_t>(TILE), tn = next(t + gridDim.x);
     const uint64_t coarse = t >> tpblog;
     uint32_t d[kItems], rk[kItems];
 #ifndef BSG_P2T_EARLY
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     }
 #pragma unroll
     for (int i = 0; i < kItems; ++i)
-      if (tid + i * kP2Threads < static_cast<int>(nv)) {
+      if (!PAD || tid + i * kP2Threads < static_cast<int>(nv)) {
         if (BSG_RANK2) atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
         else rk[i] = atomicAdd(&hist[(d[i] >> w2) & fmask], 1u);
       }
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
       __syncthreads();  // start[] read for delta before the rank atomics advance it
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
-        if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
+        if (PAD && tid + i * kP2Threads >= static_cast<int>(nv)) continue;
         const uint32_t s = SW2(atomicAdd(&start[(d[i] >> w2) & fmask], 1u));
         if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
         else sv[s] = gv[tid + i * kP2Threads];
@@ -560,7 +564,7 @@ __global__ void __launch_bounds__(kP2Threads) k_part2t(const T* __restrict__ tv,
     } else {
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
-        if (tid + i * kP2Threads >= static_cast<int>(nv)) continue;
+        if (PAD && tid + i * kP2Threads >= static_cast<int>(nv)) continue;
         const uint32_t s = SW2(start[(d[i] >> w2) & fmask] + rk[i]);
         if constexpr (BSG_P2T_EARLY) sv[s] = v[i];
         else sv[s] = gv[tid + i * kP2Threads];
@@ -1180,12 +1184,13 @@ cudaError_t run_partition(const PartitionLaunch& a, cudaStream_t s) {
   constexpr int kTile2 = sizeof(T) <= 8 ? kP2Tile : 2048;
   if constexpr (sizeof(T) <= 8 || BSG_P2T16) {
     const size_t smt = 2 * kTile2 * (sizeof(T) + 4);
-    cudaFuncSetAttribute(k_part2t<T, kTile2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
+    auto kern = (pad || !BSG_P2_FULLT) ? k_part2t<T, kTile2, true> : k_part2t<T, kTile2, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
     int per = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T, kTile2>, kP2Threads, smt);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kP2Threads, smt);
     const uint64_t tiles = n / kTile2;  // tile slots; in a padded domain the tail of every bucket is empty
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
-    k_part2t<T, kTile2><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
+    kern<<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
         tv, a.tmp_dest, p2out, a.tmp_dlow, cur2, w2, nb2, w1, static_cast<uint32_t>(tiles), pad ? cur1 : nullptr);
   }
   if constexpr (sizeof(T) <= 8) {
@@ -1413,14 +1418,15 @@ cudaError_t run_xplace(const XpartLaunch& a, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smt = 2 * kP2Tile * (sizeof(T) + 4);
-  cudaFuncSetAttribute(k_part2t<T, kP2Tile>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
+  auto kern = BSG_P2_FULLT ? k_part2t<T, kP2Tile, false> : k_part2t<T, kP2Tile, true>;  // exchange: power of two
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt));
   int per = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_part2t<T, kP2Tile>, kP2Threads, smt);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kP2Threads, smt);
   const uint64_t w1 = 1ULL << (L.Lb - L.s1);
   const uint64_t tiles = (1ULL << L.Lb) / kP2Tile;
   const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * std::max(per, 1));
   uint16_t* dlow = reinterpret_cast<uint16_t*>(me + L.dlow);
-  k_part2t<T, kP2Tile><<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
+  kern<<<static_cast<unsigned>(grid), kP2Threads, smt, s>>>(
       reinterpret_cast<const T*>(me + L.tv), reinterpret_cast<const uint32_t*>(me + L.td), static_cast<T*>(a.out),
       dlow, cur2, L.w2, 1 << L.s2, w1, static_cast<uint32_t>(tiles), nullptr);
   const size_t sm3 = (size_t{1} << L.w2) * sizeof(T);
